@@ -1,0 +1,113 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — CPU restatement of the seeded random-banded
+ * generator used for configs C3 and C5 (BASELINE.json configs[2], [4]).
+ *
+ * The reference has no such generator (its generate.py builds small
+ * triplet matrices, /root/reference/pkg/src/dacsr/generate.py:37-64); the
+ * product generates C3/C5 on the device (paper_2307_06305_b200/csrc/
+ * gen_kernels.cu) and this file is the independent checker that the device
+ * output is the documented matrix.  Every row is a pure function of
+ * (seed, row), so tests verify sampled rows of a 2^28-row device matrix
+ * without materialising it on the host.
+ *
+ * Row r of the matrix (n rows/cols, half bandwidth b, clip k to [1, kmax]):
+ *   u      = top 53 bits of H(seed, r, 0) as a double in [0,1)
+ *   k      = #{j < kmax : u >= cdf[j]}, then max(k, 1)   (Poisson via cdf table)
+ *   draw j = 1, 2, ...: t = (hi32(H(seed, r, j)) * 2b) >> 32 in [0, 2b),
+ *          off = t < b ? t - b : t - b + 1   (uniform on [-b,b] \ {0}),
+ *          rejected if already drawn, until k-1 distinct offsets;
+ *   keep offsets with 0 <= r+off < n, add the diagonal 0, sort ascending;
+ *   value(r, off) = N(H(seed ^ VALUE_SALT, r, off + b)) where
+ *   N(h) = T[i] + f * (T[i+1] - T[i]), i = h >> 52, f = ((h >> 11) & (2^41-1)) * 2^-41
+ *   with T the 4097-point normal quantile table passed in (exact IEEE ops,
+ *   compiled with -ffp-contract=off).
+ */
+#include <stdint.h>
+
+#define VALUE_SALT 0x5851F42D4C957F2DULL
+#define MAX_ROW 128
+
+static uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+static uint64_t hash3(uint64_t seed, uint64_t r, uint64_t j) {
+  return mix64(mix64(seed ^ (r * 0xD1B54A32D192ED03ULL)) + j);
+}
+
+static double quantile(uint64_t h, const double* table) {
+  uint64_t i = h >> 52;
+  double f = (double)((h >> 11) & ((1ULL << 41) - 1)) * (1.0 / 2199023255552.0);
+  double lo = table[i], hi = table[i + 1];
+  return lo + f * (hi - lo);
+}
+
+/* offsets (sorted, diagonal included) of row r; returns the count */
+int orc_gen_row(int64_t n, int64_t b, int kmax, uint64_t seed, const double* cdf,
+                int64_t r, int32_t* offs) {
+  uint64_t h0 = hash3(seed, (uint64_t)r, 0);
+  double u = (double)(h0 >> 11) * (1.0 / 9007199254740992.0);
+  int k = 0;
+  while (k < kmax && u >= cdf[k]) ++k;
+  if (k < 1) k = 1;
+  int32_t drawn[MAX_ROW];
+  int nd = 0;
+  uint64_t j = 1;
+  uint64_t span = 2ULL * (uint64_t)b;
+  while (nd < k - 1) {
+    uint64_t h = hash3(seed, (uint64_t)r, j++);
+    uint64_t t = ((h >> 32) * span) >> 32;
+    int32_t off = (int32_t)((int64_t)t < b ? (int64_t)t - b : (int64_t)t - b + 1);
+    int dup = 0;
+    for (int q = 0; q < nd; ++q) dup |= (drawn[q] == off);
+    if (!dup) drawn[nd++] = off;
+  }
+  int m = 0;
+  offs[m++] = 0;
+  for (int q = 0; q < nd; ++q) {
+    int64_t c = r + drawn[q];
+    if (c >= 0 && c < n) offs[m++] = drawn[q];
+  }
+  for (int a = 1; a < m; ++a) { /* insertion sort */
+    int32_t v = offs[a];
+    int c = a - 1;
+    while (c >= 0 && offs[c] > v) { offs[c + 1] = offs[c]; --c; }
+    offs[c + 1] = v;
+  }
+  return m;
+}
+
+double orc_gen_value(int64_t b, uint64_t seed, int64_t r, int32_t off, const double* table) {
+  return quantile(hash3(seed ^ VALUE_SALT, (uint64_t)r, (uint64_t)(off + b)), table);
+}
+
+void orc_gen_counts(int64_t n, int64_t b, int kmax, uint64_t seed, const double* cdf,
+                    int64_t r0, int64_t r1, int32_t* counts) {
+  int32_t offs[MAX_ROW];
+  for (int64_t r = r0; r < r1; ++r) counts[r - r0] = orc_gen_row(n, b, kmax, seed, cdf, r, offs);
+}
+
+/* rows [r0, r1): offsets/values written from position 0; returns entries */
+int64_t orc_gen_fill(int64_t n, int64_t b, int kmax, uint64_t seed, const double* cdf,
+                     const double* table, int64_t r0, int64_t r1, int16_t* offsets,
+                     double* values) {
+  int32_t offs[MAX_ROW];
+  int64_t pos = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    int m = orc_gen_row(n, b, kmax, seed, cdf, r, offs);
+    for (int q = 0; q < m; ++q) {
+      offsets[pos] = (int16_t)offs[q];
+      values[pos] = orc_gen_value(b, seed, r, offs[q], table);
+      ++pos;
+    }
+  }
+  return pos;
+}
+
+/* x[i] = N(H(seed, i, 0)) for i in [i0, i1) */
+void orc_gen_normal(uint64_t seed, int64_t i0, int64_t i1, const double* table, double* out) {
+  for (int64_t i = i0; i < i1; ++i) out[i - i0] = quantile(hash3(seed, (uint64_t)i, 0), table);
+}
