@@ -1,0 +1,222 @@
+/*
+ * dacsr_b200.h — C ABI of the B200 (sm_100a) DA-CSR / CSR SpMV library.
+ *
+ * The drop-in boundary for the reference's kernel plugin interface
+ * (/root/reference/pkg/src/dacsr/spmv/__init__.py:88-101 resolves
+ * `getattr(module, f"{kind}_{suffix}")` and calls
+ * `kernel(rowptr, colids, values, x, y, alpha, beta, row_start, row_end)`,
+ * _numba_kernels.py:13).  Everything here is plain pointers and sizes; all
+ * array pointers are DEVICE pointers, `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  Launches are stream-ordered and the library
+ * holds no global mutable state, so calls on different streams/devices may
+ * run concurrently.  Functions never allocate device memory: buffers (the
+ * plan's block table) are caller-owned.
+ *
+ * Arithmetic contract (identical to the reference's numba kernels):
+ * y[r] = alpha * acc_r (+ beta * y[r] iff beta != 0), acc_r accumulated in
+ * float64 from +0.0, products rounded separately (no FMA contraction); for
+ * float32 data the product is rounded to float32 before the float64
+ * accumulation and the result rounded once on the store.  beta == 0 never
+ * reads y.  With an exact order (NAIVE/MACC3/STRIP4) the result is
+ * bit-identical to the reference kernel of the same summation order.
+ */
+#ifndef DACSR_B200_H
+#define DACSR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (0 = success) ---------------------------------------- */
+enum {
+  DACSR_OK = 0,
+  DACSR_ERR_ARG = 1,     /* null pointer / bad row range / bad size        */
+  DACSR_ERR_DTYPE = 2,   /* unsupported dtype or kind combination          */
+  DACSR_ERR_VARIANT = 3, /* unknown variant or order                       */
+  DACSR_ERR_CUDA = 4,    /* CUDA runtime/launch error: dacsr_last_error()  */
+  DACSR_ERR_PLAN = 5     /* plan does not match the matrix / row range     */
+};
+
+/* ---- dtype, kind, order, variant codes ---------------------------------- */
+enum { DACSR_I8 = 0, DACSR_I16 = 1, DACSR_I32 = 2, DACSR_I64 = 3, DACSR_F32 = 4, DACSR_F64 = 5 };
+enum { DACSR_KIND_CSR = 0, DACSR_KIND_DA = 1 };
+
+/* Summation order inside a row.  NAIVE/MACC3/STRIP4 reproduce the
+ * reference kernels naive|shifted_base / multi_acc3 / strip_mined4
+ * (_numba_kernels.py:12-160) bit-for-bit.  TREE allows a lane-parallel
+ * tree combine (not bit-exact; within 2^-40 relative in tests). */
+enum { DACSR_ORDER_NAIVE = 0, DACSR_ORDER_MACC3 = 1, DACSR_ORDER_STRIP4 = 2, DACSR_ORDER_TREE = 3 };
+
+enum {
+  DACSR_VARIANT_AUTO = 0,     /* pick from the plan's row statistics             */
+  DACSR_VARIANT_ROWBLOCK = 1, /* nnz-balanced entry chunks, TMA-bulk staged,      */
+                              /* persistent; thread-per-row (exact orders),       */
+                              /* long rows cooperatively; needs a plan           */
+  DACSR_VARIANT_SCALAR = 2,   /* thread per row straight from global (exact)     */
+  DACSR_VARIANT_VECTOR2 = 3,  /* 2/4/8/16/32 lanes per row + __shfl_xor (TREE)   */
+  DACSR_VARIANT_VECTOR4 = 4,
+  DACSR_VARIANT_VECTOR8 = 5,
+  DACSR_VARIANT_VECTOR16 = 6,
+  DACSR_VARIANT_WARP = 7,
+  DACSR_VARIANT_STAGED = 8    /* fixed rows per CTA, TMA-bulk staged (no plan)   */
+};
+
+/* A matrix in CSR (absolute colids) or DA-CSR (colids = col - row) layout.
+ * rowptr: I32|I64, colids: CSR I32|I64, DA I8|I16|I32; values: F32|F64. */
+typedef struct {
+  int32_t kind;
+  int32_t rowptr_dtype;
+  int32_t colids_dtype;
+  int32_t values_dtype;
+  int64_t nrows;
+  int64_t ncols;
+  int64_t nnz;
+  const void* rowptr;
+  const void* colids;
+  const void* values;
+} dacsr_matrix_t;
+
+/* Row-length statistics of rows [row_start, row_end). */
+typedef struct {
+  int64_t rows;
+  int64_t nnz;
+  int64_t entry_start; /* rowptr[row_start] */
+  int64_t entry_end;   /* rowptr[row_end]   */
+  int64_t max_len;
+  int64_t empty_rows;
+  double mean_len;
+  double cv_len; /* coefficient of variation of row lengths */
+} dacsr_stats_t;
+
+/* nnz-balanced partition: block b stages entries
+ * [entry_base + b*cap, entry_base + (b+1)*cap) and owns the rows whose first
+ * entry falls there (rows [block_rows[b], block_rows[b+1])). */
+typedef struct {
+  int64_t row_start;
+  int64_t row_end;
+  int64_t entry_base;  /* rowptr[row_start] rounded down to 16 entries       */
+  int64_t entry_end;   /* rowptr[row_end]                                     */
+  int64_t nblocks;
+  int32_t cap;         /* entries per block (multiple of 16)                  */
+  int32_t long_len;    /* rows longer than this are reduced by the whole CTA  */
+  const int64_t* block_rows; /* device, nblocks + 1 entries (caller-owned)    */
+} dacsr_plan_t;
+
+const char* dacsr_version(void);
+/* Text of the last CUDA error seen by this thread ("" if none). */
+const char* dacsr_last_error(void);
+
+/* Row statistics (reads rowptr on the device; synchronizes `stream`).
+ * scratch_dev: caller-owned device buffer of DACSR_ANALYZE_SCRATCH bytes. */
+#define DACSR_ANALYZE_SCRATCH 64
+int dacsr_analyze(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end,
+                  void* scratch_dev, dacsr_stats_t* out, void* stream);
+
+/* Default block capacity for a matrix with these statistics. */
+int32_t dacsr_plan_default_cap(const dacsr_stats_t* stats, int32_t values_dtype,
+                               int32_t colids_dtype);
+/* Number of blocks a plan of capacity `cap` needs (size block_rows as +1). */
+int64_t dacsr_plan_nblocks(const dacsr_matrix_t* a, int64_t entry_start, int64_t entry_end,
+                           int32_t cap);
+/* Fill `block_rows_dev` (nblocks + 1 int64) and `out`.  entry_start/end are
+ * rowptr[row_start], rowptr[row_end] (known to the caller from analyze). */
+int dacsr_plan_build(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end,
+                     int64_t entry_start, int64_t entry_end, int32_t cap, int32_t long_len,
+                     int64_t* block_rows_dev, dacsr_plan_t* out, void* stream);
+
+/* Variant the library would run for DACSR_VARIANT_AUTO. */
+int32_t dacsr_select_variant(const dacsr_stats_t* stats, int32_t order);
+
+/* y[r] = alpha * sum_i values[i] * x[col_i + x_offset] (+ beta*y[r]) for
+ * r in [row_start, row_end), col_i = colids[i] (CSR) or r + colids[i] (DA).
+ * `plan` may be NULL except for DACSR_VARIANT_ROWBLOCK (AUTO falls back to
+ * STAGED without a plan).  x_offset shifts x addressing (a rank-local halo
+ * buffer); 0 for a plain SpMV. */
+int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t variant,
+               int32_t order, const void* x, int64_t x_offset, void* y, double alpha,
+               double beta, int64_t row_start, int64_t row_end, void* stream);
+
+/* The reference's alpha == 0 short-cut (spmv/__init__.py:150-156):
+ * y = 0 if beta == 0, y = (T)((double)beta * y) if beta not in {0, 1}. */
+int dacsr_scale(void* y, int32_t values_dtype, int64_t n, double beta, void* stream);
+
+/* Deterministic sum of squares: partial[c] = sum over rows [c*chunk,
+ * (c+1)*chunk) ∩ [0, n) of y^2 (fixed tree per chunk, independent of how
+ * rows are spread over ranks when rank boundaries are chunk-aligned). */
+int dacsr_sumsq_chunks(const void* y, int32_t values_dtype, int64_t n, int64_t chunk,
+                       double* partial, void* stream);
+/* out[0] = sum of partial[0..m) in index order (one thread, exact order). */
+int dacsr_sum_ordered(const double* partial, int64_t m, double* out, void* stream);
+
+/* Reference-named kernel entry points (one per _numba_kernels.py function;
+ * int32 rowptr, DA int16 offsets / CSR int32 colids, the paper's layout).
+ * Exact order of the named reference kernel; no plan needed. */
+#define DACSR_DECLARE_TYPED(KIND, CI, NAME, VT, VN)                                       \
+  int dacsr_##KIND##_##NAME##_##VN(const int32_t* rowptr, const CI* colids,               \
+                                   const VT* values, const VT* x, VT* y, double alpha,    \
+                                   double beta, int64_t row_start, int64_t row_end,       \
+                                   void* stream);
+#define DACSR_DECLARE_KIND(KIND, CI)                          \
+  DACSR_DECLARE_TYPED(KIND, CI, naive, double, f64)           \
+  DACSR_DECLARE_TYPED(KIND, CI, shifted_base, double, f64)    \
+  DACSR_DECLARE_TYPED(KIND, CI, multi_acc3, double, f64)      \
+  DACSR_DECLARE_TYPED(KIND, CI, strip_mined4, double, f64)    \
+  DACSR_DECLARE_TYPED(KIND, CI, naive, float, f32)            \
+  DACSR_DECLARE_TYPED(KIND, CI, shifted_base, float, f32)     \
+  DACSR_DECLARE_TYPED(KIND, CI, multi_acc3, float, f32)       \
+  DACSR_DECLARE_TYPED(KIND, CI, strip_mined4, float, f32)
+DACSR_DECLARE_KIND(csr, int32_t)
+DACSR_DECLARE_KIND(da, int16_t)
+
+/* ---- device-side conversion (reference core.py:320-355) ------------------ */
+/* max |col - row| over the entries of a CSR or DA-CSR matrix into the
+ * device int64 *out_dev (0 if empty); stream-ordered, no synchronization. */
+int dacsr_bandwidth(const dacsr_matrix_t* a, int64_t* out_dev, void* stream);
+/* offsets[i] = colids[i] - row(i) into an int8/int16/int32 array; caller
+ * checks the bandwidth first (BandwidthExceedsIndexRange is host logic). */
+int dacsr_csr_to_da(const dacsr_matrix_t* a, void* offsets, int32_t offsets_dtype,
+                    void* stream);
+
+/* ---- seeded C3/C5 generator (oracle: oracle/gen_oracle.c) ----------------- */
+/* counts[r - r0] = entries of row r (diagonal included). */
+int dacsr_gen_banded_counts(int64_t n, int64_t b, int32_t kmax, uint64_t seed,
+                            const double* cdf_dev, int64_t r0, int64_t r1, int32_t* counts,
+                            void* stream);
+/* Fill rows [r0, r1) given their (local, from 0) rowptr; DA offsets and/or
+ * CSR colids (either may be NULL), f64 or f32 values. */
+int dacsr_gen_banded_fill(int64_t n, int64_t b, int32_t kmax, uint64_t seed,
+                          const double* cdf_dev, const double* table_dev, int64_t r0,
+                          int64_t r1, const void* rowptr, int32_t rowptr_dtype,
+                          int16_t* offsets, int32_t* colids, void* values,
+                          int32_t values_dtype, void* stream);
+/* out[i - i0] = N(H(seed, i, 0)) for i in [i0, i1). */
+int dacsr_gen_normal(uint64_t seed, int64_t i0, int64_t i1, const double* table_dev,
+                     void* out, int32_t values_dtype, void* stream);
+/* Inclusive-exclusive scan helper: rowptr[0] = 0, rowptr[k+1] = sum counts[0..k]
+ * into int32 or int64 (uses a caller-provided temp buffer of temp_bytes;
+ * query with temp == NULL). */
+int dacsr_counts_to_rowptr(const int32_t* counts, int64_t m, void* rowptr,
+                           int32_t rowptr_dtype, void* temp, size_t* temp_bytes,
+                           void* stream);
+
+/* ---- host-side reordering (reference reorder.py:70-220), CPU only -------- */
+/* Symmetrized adjacency of a square CSR pattern (pattern of A + A^T, no
+ * self-loops, ascending, deduplicated).  Two calls: first with
+ * indices == NULL to get indptr and the count; then with indices. */
+int dacsr_host_adjacency(int64_t n, const int64_t* rowptr, const int64_t* colids,
+                         int64_t* indptr, int64_t* indices);
+/* Reverse Cuthill–McKee with the reference's tie-breaking; perm[new] = old. */
+int dacsr_host_rcm(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* perm);
+/* P A P^T in canonical CSR: rows/cols relabelled through inv (old -> new),
+ * values carried as raw bytes of width value_bytes; out arrays int64. */
+int dacsr_host_permute(int64_t n, const int64_t* rowptr, const int64_t* colids,
+                       const void* values, int32_t value_bytes, const int64_t* perm,
+                       int64_t* out_rowptr, int64_t* out_colids, void* out_values);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DACSR_B200_H */

@@ -1,0 +1,334 @@
+// Analysis, planning and small utility kernels of the C ABI:
+//   dacsr_analyze          row-length statistics (selection heuristic input)
+//   dacsr_plan_*           nnz-balanced chunk partition for ROWBLOCK
+//   dacsr_scale            the reference's alpha == 0 short-cut on device
+//   dacsr_sumsq_chunks     deterministic per-chunk sum of y^2 (power iteration)
+//   dacsr_sum_ordered      ordered fold of the chunk partials
+//   dacsr_bandwidth        max |col - row|   (reference core.py:320-331)
+//   dacsr_csr_to_da        colids - row      (reference core.py:352-353)
+
+#include <algorithm>
+#include <cmath>
+
+#include "device_common.cuh"
+
+namespace dacsr {
+namespace {
+
+template <class RP>
+__device__ __forceinline__ int64_t rp_at(const void* rp, int64_t i) {
+  return static_cast<int64_t>(ldg(static_cast<const RP*>(rp) + i));
+}
+
+struct AnalyzeScratch {
+  unsigned long long max_len;
+  unsigned long long empty;
+  double sum_sq;
+  int64_t e0, e1;
+};
+
+template <class RP>
+__global__ void analyze_kernel(const void* rp, int64_t rs, int64_t re, AnalyzeScratch* out) {
+  unsigned long long mx = 0, empty = 0;
+  double sq = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = rs + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < re;
+       r += stride) {
+    const int64_t len = rp_at<RP>(rp, r + 1) - rp_at<RP>(rp, r);
+    mx = max(mx, static_cast<unsigned long long>(len));
+    empty += len == 0;
+    sq += static_cast<double>(len) * static_cast<double>(len);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    empty += __shfl_xor_sync(0xffffffffu, empty, o);
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&out->max_len, mx);
+    atomicAdd(&out->empty, empty);
+    atomicAdd(&out->sum_sq, sq);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out->e0 = rp_at<RP>(rp, rs);
+    out->e1 = rp_at<RP>(rp, re);
+  }
+}
+
+template <class RP>
+__global__ void plan_kernel(const void* rp, int64_t rs, int64_t re, int64_t base, int64_t cap,
+                            int64_t nblocks, int64_t* block_rows) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b > nblocks) return;
+  if (b == 0) {
+    block_rows[0] = rs;
+    return;
+  }
+  if (b == nblocks) {
+    block_rows[b] = re;
+    return;
+  }
+  // first row r in [rs, re] with rowptr[r] >= base + b*cap
+  const int64_t target = base + b * cap;
+  int64_t lo = rs, hi = re;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (rp_at<RP>(rp, mid) < target) lo = mid + 1;
+    else hi = mid;
+  }
+  block_rows[b] = lo;
+}
+
+template <class VT>
+__global__ void scale_kernel(VT* y, int64_t n, double beta) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    if (beta == 0.0) y[i] = VT(0);
+    else store_rounded(y + i, __dmul_rn(beta, to_f64(y[i])));
+  }
+}
+
+// one CTA per chunk; fixed strided assignment + fixed tree => deterministic
+template <class VT>
+__global__ void __launch_bounds__(256) sumsq_kernel(const VT* y, int64_t n, int64_t chunk,
+                                                    double* partial) {
+  __shared__ double red[8];
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t c1 = min(n, c0 + chunk);
+  double acc = 0.0;
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    const double v = to_f64(y[i]);
+    acc = __dadd_rn(acc, __dmul_rn(v, v));
+  }
+  for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (blockDim.x >> 5); ++w) t = __dadd_rn(t, red[w]);
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_ordered_kernel(const double* p, int64_t m, double* out) {
+  double t = 0.0;
+  for (int64_t i = 0; i < m; ++i) t = __dadd_rn(t, p[i]);
+  *out = t;
+}
+
+// warp per row
+template <int KIND, class RP, class CI>
+__global__ void bandwidth_kernel(const void* rpv, const CI* ci, int64_t nrows,
+                                 unsigned long long* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long mx = 0;
+  for (int64_t r = warp; r < nrows; r += nw) {
+    const int64_t b = rp_at<RP>(rpv, r), e = rp_at<RP>(rpv, r + 1);
+    for (int64_t i = b + lane; i < e; i += 32) {
+      const int64_t c = static_cast<int64_t>(ldg(ci + i));
+      const int64_t off = KIND == DACSR_KIND_DA ? c : c - r;
+      mx = max(mx, static_cast<unsigned long long>(off < 0 ? -off : off));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0 && mx) atomicMax(out, mx);
+}
+
+template <class RP, class CI, class OT>
+__global__ void to_da_kernel(const void* rpv, const CI* ci, int64_t nrows, OT* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < nrows; r += nw) {
+    const int64_t b = rp_at<RP>(rpv, r), e = rp_at<RP>(rpv, r + 1);
+    for (int64_t i = b + lane; i < e; i += 32)
+      out[i] = static_cast<OT>(static_cast<int64_t>(ldg(ci + i)) - r);
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  const int64_t g = (work + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32)));
+}
+
+int cuda_status(const char* what, cudaError_t e) {
+  if (e != cudaSuccess) {
+    set_last_error(what, e);
+    return DACSR_ERR_CUDA;
+  }
+  return DACSR_OK;
+}
+
+template <class CI>
+int launch_bandwidth(const dacsr_matrix_t* a, unsigned long long* out, cudaStream_t st) {
+  const int g = grid_for(a->nrows * 32, 256);
+  const bool da = a->kind == DACSR_KIND_DA;
+  const bool r64 = a->rowptr_dtype == DACSR_I64;
+  const CI* ci = static_cast<const CI*>(a->colids);
+  if (da && r64) bandwidth_kernel<DACSR_KIND_DA, int64_t, CI><<<g, 256, 0, st>>>(a->rowptr, ci, a->nrows, out);
+  else if (da) bandwidth_kernel<DACSR_KIND_DA, int32_t, CI><<<g, 256, 0, st>>>(a->rowptr, ci, a->nrows, out);
+  else if (r64) bandwidth_kernel<DACSR_KIND_CSR, int64_t, CI><<<g, 256, 0, st>>>(a->rowptr, ci, a->nrows, out);
+  else bandwidth_kernel<DACSR_KIND_CSR, int32_t, CI><<<g, 256, 0, st>>>(a->rowptr, ci, a->nrows, out);
+  return check_launch("bandwidth_kernel");
+}
+
+template <class RP, class CI>
+int launch_to_da(const dacsr_matrix_t* a, void* out, int32_t odt, cudaStream_t st) {
+  const int g = grid_for(a->nrows * 32, 256);
+  const CI* ci = static_cast<const CI*>(a->colids);
+  switch (odt) {
+    case DACSR_I8: to_da_kernel<RP, CI, int8_t><<<g, 256, 0, st>>>(a->rowptr, ci, a->nrows, static_cast<int8_t*>(out)); break;
+    case DACSR_I16: to_da_kernel<RP, CI, int16_t><<<g, 256, 0, st>>>(a->rowptr, ci, a->nrows, static_cast<int16_t*>(out)); break;
+    case DACSR_I32: to_da_kernel<RP, CI, int32_t><<<g, 256, 0, st>>>(a->rowptr, ci, a->nrows, static_cast<int32_t*>(out)); break;
+    default: return DACSR_ERR_DTYPE;
+  }
+  return check_launch("to_da_kernel");
+}
+
+}  // namespace
+}  // namespace dacsr
+
+using namespace dacsr;
+
+extern "C" {
+
+int dacsr_analyze(const dacsr_matrix_t* a, int64_t rs, int64_t re, void* scratch,
+                  dacsr_stats_t* out, void* stream) {
+  if (!a || !out || !scratch || !a->rowptr || rs < 0 || re < rs || re > a->nrows)
+    return DACSR_ERR_ARG;
+  auto st = static_cast<cudaStream_t>(stream);
+  auto* sc = static_cast<AnalyzeScratch*>(scratch);
+  int rc = cuda_status("analyze memset", cudaMemsetAsync(sc, 0, sizeof(AnalyzeScratch), st));
+  if (rc) return rc;
+  const int g = grid_for(std::max<int64_t>(re - rs, 1), 256);
+  if (a->rowptr_dtype == DACSR_I64) analyze_kernel<int64_t><<<g, 256, 0, st>>>(a->rowptr, rs, re, sc);
+  else if (a->rowptr_dtype == DACSR_I32) analyze_kernel<int32_t><<<g, 256, 0, st>>>(a->rowptr, rs, re, sc);
+  else return DACSR_ERR_DTYPE;
+  if ((rc = check_launch("analyze_kernel"))) return rc;
+  AnalyzeScratch h;
+  if ((rc = cuda_status("analyze copy", cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st))))
+    return rc;
+  if ((rc = cuda_status("analyze sync", cudaStreamSynchronize(st)))) return rc;
+  const int64_t rows = re - rs;
+  out->rows = rows;
+  out->entry_start = h.e0;
+  out->entry_end = h.e1;
+  out->nnz = h.e1 - h.e0;
+  out->max_len = static_cast<int64_t>(h.max_len);
+  out->empty_rows = static_cast<int64_t>(h.empty);
+  out->mean_len = rows ? static_cast<double>(out->nnz) / rows : 0.0;
+  const double var = rows ? h.sum_sq / rows - out->mean_len * out->mean_len : 0.0;
+  out->cv_len = out->mean_len > 0 ? std::sqrt(std::max(var, 0.0)) / out->mean_len : 0.0;
+  return DACSR_OK;
+}
+
+int32_t dacsr_plan_default_cap(const dacsr_stats_t* s, int32_t values_dtype, int32_t colids_dtype) {
+  static const int kBytes[6] = {1, 2, 4, 8, 4, 8};
+  if (!s || values_dtype < 0 || values_dtype > 5 || colids_dtype < 0 || colids_dtype > 5) return 2048;
+  const int per = kBytes[values_dtype] + kBytes[colids_dtype];
+  // about 0.9 rows per thread of a 512-thread CTA, >= 2 stages in 100 KiB
+  double cap = 0.9 * 512.0 * std::max(s->mean_len, 1.0);
+  cap = std::min(cap, std::min(8192.0, 51200.0 / per));
+  cap = std::max(cap, 512.0);
+  return static_cast<int32_t>(cap) & ~15;
+}
+
+int64_t dacsr_plan_nblocks(const dacsr_matrix_t* a, int64_t e0, int64_t e1, int32_t cap) {
+  (void)a;
+  if (cap <= 0) return 0;
+  const int64_t base = e0 & ~int64_t(15);
+  return std::max<int64_t>(1, (e1 - base + cap - 1) / cap);
+}
+
+int dacsr_plan_build(const dacsr_matrix_t* a, int64_t rs, int64_t re, int64_t e0, int64_t e1,
+                     int32_t cap, int32_t long_len, int64_t* block_rows, dacsr_plan_t* out,
+                     void* stream) {
+  if (!a || !out || !block_rows || cap <= 0 || (cap & 15) || rs < 0 || re < rs || re > a->nrows)
+    return DACSR_ERR_ARG;
+  auto st = static_cast<cudaStream_t>(stream);
+  const int64_t base = e0 & ~int64_t(15);
+  const int64_t nb = dacsr_plan_nblocks(a, e0, e1, cap);
+  const int g = static_cast<int>((nb + 1 + 255) / 256);
+  if (a->rowptr_dtype == DACSR_I64)
+    plan_kernel<int64_t><<<g, 256, 0, st>>>(a->rowptr, rs, re, base, cap, nb, block_rows);
+  else if (a->rowptr_dtype == DACSR_I32)
+    plan_kernel<int32_t><<<g, 256, 0, st>>>(a->rowptr, rs, re, base, cap, nb, block_rows);
+  else
+    return DACSR_ERR_DTYPE;
+  int rc = check_launch("plan_kernel");
+  if (rc) return rc;
+  out->row_start = rs;
+  out->row_end = re;
+  out->entry_base = base;
+  out->entry_end = e1;
+  out->nblocks = nb;
+  out->cap = cap;
+  out->long_len = std::max<int32_t>(long_len, cap / 62);
+  out->block_rows = block_rows;
+  return DACSR_OK;
+}
+
+int dacsr_scale(void* y, int32_t vdt, int64_t n, double beta, void* stream) {
+  if (n < 0 || (n > 0 && !y)) return DACSR_ERR_ARG;
+  if (n == 0 || beta == 1.0) return DACSR_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const int g = grid_for(n, 256);
+  if (vdt == DACSR_F64) scale_kernel<double><<<g, 256, 0, st>>>(static_cast<double*>(y), n, beta);
+  else if (vdt == DACSR_F32) scale_kernel<float><<<g, 256, 0, st>>>(static_cast<float*>(y), n, beta);
+  else return DACSR_ERR_DTYPE;
+  return check_launch("scale_kernel");
+}
+
+int dacsr_sumsq_chunks(const void* y, int32_t vdt, int64_t n, int64_t chunk, double* partial,
+                       void* stream) {
+  if (n < 0 || chunk <= 0 || !partial || (n > 0 && !y)) return DACSR_ERR_ARG;
+  if (n == 0) return DACSR_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const int64_t m = (n + chunk - 1) / chunk;
+  if (m > 0x7fffffff) return DACSR_ERR_ARG;
+  if (vdt == DACSR_F64) sumsq_kernel<double><<<static_cast<unsigned>(m), 256, 0, st>>>(static_cast<const double*>(y), n, chunk, partial);
+  else if (vdt == DACSR_F32) sumsq_kernel<float><<<static_cast<unsigned>(m), 256, 0, st>>>(static_cast<const float*>(y), n, chunk, partial);
+  else return DACSR_ERR_DTYPE;
+  return check_launch("sumsq_kernel");
+}
+
+int dacsr_sum_ordered(const double* partial, int64_t m, double* out, void* stream) {
+  if (!out || m < 0 || (m > 0 && !partial)) return DACSR_ERR_ARG;
+  sum_ordered_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(partial, m, out);
+  return check_launch("sum_ordered_kernel");
+}
+
+int dacsr_bandwidth(const dacsr_matrix_t* a, int64_t* out, void* stream) {
+  if (!a || !out || !a->rowptr || (a->nnz > 0 && !a->colids)) return DACSR_ERR_ARG;
+  auto st = static_cast<cudaStream_t>(stream);
+  int rc = cuda_status("bandwidth memset", cudaMemsetAsync(out, 0, sizeof(int64_t), st));
+  if (rc || a->nrows == 0) return rc;
+  auto* o = reinterpret_cast<unsigned long long*>(out);
+  switch (a->colids_dtype) {
+    case DACSR_I8: return launch_bandwidth<int8_t>(a, o, st);
+    case DACSR_I16: return launch_bandwidth<int16_t>(a, o, st);
+    case DACSR_I32: return launch_bandwidth<int32_t>(a, o, st);
+    case DACSR_I64: return launch_bandwidth<int64_t>(a, o, st);
+    default: return DACSR_ERR_DTYPE;
+  }
+}
+
+int dacsr_csr_to_da(const dacsr_matrix_t* a, void* offsets, int32_t odt, void* stream) {
+  if (!a || a->kind != DACSR_KIND_CSR || !a->rowptr || (a->nnz > 0 && (!a->colids || !offsets)))
+    return DACSR_ERR_ARG;
+  if (a->nrows == 0) return DACSR_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const bool r64 = a->rowptr_dtype == DACSR_I64;
+  switch (a->colids_dtype) {
+    case DACSR_I32: return r64 ? launch_to_da<int64_t, int32_t>(a, offsets, odt, st)
+                               : launch_to_da<int32_t, int32_t>(a, offsets, odt, st);
+    case DACSR_I64: return r64 ? launch_to_da<int64_t, int64_t>(a, offsets, odt, st)
+                               : launch_to_da<int32_t, int64_t>(a, offsets, odt, st);
+    default: return DACSR_ERR_DTYPE;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,538 @@
+// SpMV kernels for CSR and DA-CSR on sm_100a, and their C-ABI launchers.
+//
+// Replaces the reference's compiled inner loops
+// (/root/reference/pkg/src/dacsr/spmv/_numba_kernels.py:12-160) behind the
+// kernel-plugin boundary (spmv/__init__.py:88-101).  Kernel family:
+//
+//  ROWBLOCK  persistent, nnz-balanced.  Entry chunk b = [base + b*cap,
+//            base + (b+1)*cap) is streamed into shared memory by the TMA
+//            bulk-copy engine (cp.async.bulk + mbarrier, `stages`-deep ring
+//            per CTA, no register staging) — values and offsets are the
+//            ~93% of the bytes and move as a pure memcpy.  The rows whose
+//            first entry lies in the chunk (plan.block_rows) are reduced one
+//            thread per row in the reference's exact order; the few entries
+//            of a row that spill past the chunk are read from global.  Rows
+//            longer than long_len are reduced by the whole CTA (exact:
+//            products staged in smem, one thread sums in order, pipelined;
+//            TREE: block tree).
+//  STAGED    the same row engine with fixed rows per CTA and a one-shot bulk
+//            copy; needs no plan (the reference-named entry points).
+//  SCALAR    thread per row straight from global (exact orders).
+//  VECTOR<G> G lanes per row, lane-strided partial sums, __shfl_xor tree.
+//
+// Column of entry i in row r: CSR colids[i]; DA r + colids[i] (the shifted
+// base of PAPER.md Snippet 2); plus x_offset for rank-local halo buffers.
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "device_common.cuh"
+
+namespace dacsr {
+
+constexpr int kMaxThreads = 512;
+constexpr int kMaxStages = 4;
+constexpr int kMaxLong = 64;      // rows > long_len starting in one chunk (<= cap/long_len+1)
+constexpr int kLongChunk = 512;   // products per cooperative round (x2 buffers)
+constexpr int kScratchBytes = 2 * kLongChunk * 8;
+
+// ------------------------------------------------------------- error state
+namespace {
+thread_local char g_last_error[256] = "";
+}
+
+void set_last_error(const char* what, cudaError_t e) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%d)", what, cudaGetErrorString(e),
+           static_cast<int>(e));
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_error(what, e);
+    return DACSR_ERR_CUDA;
+  }
+  return DACSR_OK;
+}
+
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------- kernel args
+template <int KIND, class RP, class CI, class VT>
+struct Mat {
+  const RP* __restrict__ rp;
+  const CI* __restrict__ ci;
+  const VT* __restrict__ v;
+  const VT* __restrict__ x;
+  VT* __restrict__ y;
+  int64_t xoff;
+  __device__ __forceinline__ int64_t col(int64_t r, CI c) const {
+    return (KIND == DACSR_KIND_DA ? r + static_cast<int64_t>(c) : static_cast<int64_t>(c)) +
+           xoff;
+  }
+  __device__ __forceinline__ double prod_global(int64_t r, int64_t i) const {
+    return product(ldg(v + i), ldg(x + col(r, ldg(ci + i))));
+  }
+};
+
+struct Scal {
+  double alpha, beta;
+  int order;
+  int64_t long_len;
+};
+
+struct Chunks {
+  const int64_t* block_rows;
+  int64_t base, end, nblocks;
+  int cap, stages;
+};
+
+// --------------------------------------------------- block reduce (TREE)
+__device__ __forceinline__ double block_sum_tree(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < nw ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+  }
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+// Entry i of row r as seen by a CTA whose chunk [lo, hi) sits in smem.
+template <int KIND, class RP, class CI, class VT>
+struct StagedGet {
+  const Mat<KIND, RP, CI, VT>& m;
+  const VT* sv;
+  const CI* si;
+  int64_t lo, hi, r;
+  __device__ __forceinline__ double operator()(int64_t i) const {
+    if (i < hi) {
+      const int k = static_cast<int>(i - lo);
+      return product(sv[k], ldg(m.x + m.col(r, si[k])));
+    }
+    return m.prod_global(r, i);
+  }
+};
+
+// One long row, reduced by the whole CTA.
+template <int KIND, class RP, class CI, class VT>
+__device__ void long_row(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int64_t r, int64_t lo,
+                         int64_t hi, const VT* sv, const CI* si, double* scratch) {
+  const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1), len = e - b;
+  StagedGet<KIND, RP, CI, VT> get{m, sv, si, lo, hi, r};
+  if (s.order == DACSR_ORDER_TREE) {
+    double part = 0.0;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) part = __dadd_rn(part, get(i));
+    const double t = block_sum_tree(part, scratch);
+    if (threadIdx.x == 0) epilogue(m.y, r, t, s.alpha, s.beta);
+    __syncthreads();
+    return;
+  }
+  // exact: warps 1.. produce products of round c+1 while thread 0 folds
+  // round c in the reference order.
+  const int64_t rounds = (len + kLongChunk - 1) / kLongChunk;
+  const int producers = blockDim.x - 32;
+  const int pid = threadIdx.x - 32;
+  auto produce = [&](int64_t c) {
+    double* buf = scratch + (c & 1) * kLongChunk;
+    const int64_t start = b + c * kLongChunk;
+    const int n = static_cast<int>(min64(kLongChunk, e - start));
+    for (int k = pid; k < n; k += producers) buf[k] = get(start + k);
+  };
+  OrderedAcc acc;
+  if (threadIdx.x == 0) acc.init(s.order, len);
+  if (pid >= 0 && rounds > 0) produce(0);
+  __syncthreads();
+  for (int64_t c = 0; c < rounds; ++c) {
+    if (pid >= 0 && c + 1 < rounds) produce(c + 1);
+    if (threadIdx.x == 0) {
+      const double* buf = scratch + (c & 1) * kLongChunk;
+      const int64_t start = c * kLongChunk;
+      const int n = static_cast<int>(min64(kLongChunk, len - start));
+      for (int k = 0; k < n; ++k) acc.add(start + k, buf[k]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) epilogue(m.y, r, acc.result(), s.alpha, s.beta);
+  __syncthreads();
+}
+
+// Rows [r0, r1) whose entries are (mostly) staged in smem at [lo, hi).
+// Ends after a __syncthreads: the stage may be overwritten afterwards.
+template <int KIND, class RP, class CI, class VT>
+__device__ void process_rows(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int64_t r0,
+                             int64_t r1, int64_t lo, int64_t hi, const VT* sv, const CI* si,
+                             int64_t* long_rows, int* n_long, double* scratch) {
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1);
+    if (e - b > s.long_len) {
+      long_rows[atomicAdd(n_long, 1)] = r;
+      continue;
+    }
+    StagedGet<KIND, RP, CI, VT> get{m, sv, si, lo, hi, r};
+    epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
+  }
+  __syncthreads();
+  const int nl = *n_long;
+  for (int k = 0; k < nl; ++k) long_row(m, s, long_rows[k], lo, hi, sv, si, scratch);
+}
+
+// ------------------------------------------------- ROWBLOCK (persistent)
+template <int KIND, class RP, class CI, class VT>
+__global__ void __launch_bounds__(kMaxThreads, 2)
+    rowblock_kernel(Mat<KIND, RP, CI, VT> m, Scal s, Chunks p) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ int64_t long_rows[kMaxLong];
+  __shared__ int n_long;
+
+  const int64_t nb = p.nblocks;
+  if (blockIdx.x >= nb) return;
+  const int64_t mine = (nb - 1 - blockIdx.x) / gridDim.x + 1;
+  const int cap = p.cap, stages = p.stages;
+  const size_t vbytes = static_cast<size_t>(cap) * sizeof(VT);
+  const size_t stage_bytes = static_cast<size_t>(cap) * (sizeof(VT) + sizeof(CI));
+  double* scratch = reinterpret_cast<double*>(dsm + stages * stage_bytes);
+  const int64_t copy_end = p.end & ~int64_t(15);
+
+  auto lo_of = [&](int64_t b) { return p.base + b * cap; };
+  auto hi_of = [&](int64_t b) {
+    const int64_t lo = lo_of(b), hi = min(lo + cap, copy_end);
+    return hi > lo ? hi : lo;
+  };
+  auto issue = [&](int64_t k) {
+    const int64_t b = blockIdx.x + k * gridDim.x;
+    const int st = static_cast<int>(k % stages);
+    const int64_t lo = lo_of(b), hi = hi_of(b);
+    if (hi > lo) {
+      const uint32_t n = static_cast<uint32_t>(hi - lo);
+      unsigned char* dst = dsm + st * stage_bytes;
+      mbar_arrive_expect_tx(&full[st], n * static_cast<uint32_t>(sizeof(VT) + sizeof(CI)));
+      bulk_copy_g2s(dst, m.v + lo, n * sizeof(VT), &full[st]);
+      bulk_copy_g2s(dst + vbytes, m.ci + lo, n * sizeof(CI), &full[st]);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < stages; ++st) mbar_init(&full[st], 1);
+    mbar_fence_init();
+    n_long = 0;
+    for (int64_t k = 0; k < min64(stages, mine); ++k) issue(k);
+  }
+  __syncthreads();
+
+  for (int64_t k = 0; k < mine; ++k) {
+    const int64_t b = blockIdx.x + k * gridDim.x;
+    const int st = static_cast<int>(k % stages);
+    const int64_t r0 = ldg(p.block_rows + b), r1 = ldg(p.block_rows + b + 1);
+    const int64_t lo = lo_of(b), hi = hi_of(b);
+    if (hi > lo) mbar_wait(&full[st], static_cast<uint32_t>((k / stages) & 1));
+    const unsigned char* stage = dsm + st * stage_bytes;
+    process_rows(m, s, r0, r1, lo, hi, reinterpret_cast<const VT*>(stage),
+                 reinterpret_cast<const CI*>(stage + vbytes), long_rows, &n_long, scratch);
+    if (threadIdx.x == 0) {
+      n_long = 0;
+      if (k + stages < mine) {
+        fence_proxy_async_smem();
+        issue(k + stages);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------- STAGED (fixed rows per CTA)
+template <int KIND, class RP, class CI, class VT>
+__global__ void __launch_bounds__(256, 4)
+    staged_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t row_start, int64_t row_end, int scap) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int64_t long_rows[256];
+  __shared__ int n_long;
+  __shared__ int64_t s_lo, s_hi;
+
+  const int64_t r0 = row_start + static_cast<int64_t>(blockIdx.x) * blockDim.x;
+  const int64_t r1 = min64(r0 + blockDim.x, row_end);
+  const size_t vbytes = static_cast<size_t>(scap) * sizeof(VT);
+  double* scratch = reinterpret_cast<double*>(dsm + static_cast<size_t>(scap) * (sizeof(VT) + sizeof(CI)));
+  if (threadIdx.x == 0) {
+    const int64_t e0 = ldg(m.rp + r0), e1 = ldg(m.rp + r1);
+    const int64_t lo = e0 & ~int64_t(15);
+    int64_t hi = min64(e1 & ~int64_t(15), lo + scap);
+    if (hi < lo) hi = lo;
+    s_lo = lo;
+    s_hi = hi;
+    n_long = 0;
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    if (hi > lo) {
+      const uint32_t n = static_cast<uint32_t>(hi - lo);
+      mbar_arrive_expect_tx(&bar, n * static_cast<uint32_t>(sizeof(VT) + sizeof(CI)));
+      bulk_copy_g2s(dsm, m.v + lo, n * sizeof(VT), &bar);
+      bulk_copy_g2s(dsm + vbytes, m.ci + lo, n * sizeof(CI), &bar);
+    }
+  }
+  __syncthreads();
+  const int64_t lo = s_lo, hi = s_hi;
+  if (hi > lo) mbar_wait(&bar, 0);
+  process_rows(m, s, r0, r1, lo, hi, reinterpret_cast<const VT*>(dsm),
+               reinterpret_cast<const CI*>(dsm + vbytes), long_rows, &n_long, scratch);
+}
+
+// ----------------------------------------------------------- SCALAR
+template <int KIND, class RP, class CI, class VT>
+__global__ void __launch_bounds__(256)
+    scalar_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t row_start, int64_t row_end) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = row_start + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       r < row_end; r += stride) {
+    const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1);
+    auto get = [&](int64_t i) { return m.prod_global(r, i); };
+    epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
+  }
+}
+
+// ----------------------------------------------------------- VECTOR<G>
+template <int G, int KIND, class RP, class CI, class VT>
+__global__ void __launch_bounds__(256)
+    vector_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t row_start, int64_t row_end) {
+  constexpr int kGroups = 32 / G;
+  const int lane = threadIdx.x & 31, sub = lane % G, grp = lane / G;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t base = row_start + warp * kGroups; base < row_end; base += nwarps * kGroups) {
+    const int64_t r = base + grp;
+    double acc = 0.0;
+    int64_t b = 0, e = 0;
+    if (r < row_end) {
+      b = ldg(m.rp + r);
+      e = ldg(m.rp + r + 1);
+    }
+    for (int64_t i = b + sub; i < e; i += G) acc = __dadd_rn(acc, m.prod_global(r, i));
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (sub == 0 && r < row_end) epilogue(m.y, r, acc, s.alpha, s.beta);
+  }
+}
+
+// ============================================================ host side
+namespace {
+
+int sm_count() {
+  static int cached = -1;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cached < 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cached = v;
+  }
+  return cached;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct Req {
+  const dacsr_plan_t* plan;
+  int variant, order;
+  const void* x;
+  int64_t xoff;
+  void* y;
+  double alpha, beta;
+  int64_t rs, re;
+  cudaStream_t stream;
+};
+
+template <class VT, class CI>
+int rowblock_stages(int cap) {
+  const size_t stage = static_cast<size_t>(cap) * (sizeof(VT) + sizeof(CI));
+  const size_t budget = 100 * 1024;
+  int st = static_cast<int>(budget / stage);
+  return std::max(2, std::min(kMaxStages, st));
+}
+
+template <int KIND, class RP, class CI, class VT>
+int launch(const dacsr_matrix_t* a, const Req& q) {
+  Mat<KIND, RP, CI, VT> m{static_cast<const RP*>(a->rowptr), static_cast<const CI*>(a->colids),
+                          static_cast<const VT*>(a->values), static_cast<const VT*>(q.x),
+                          static_cast<VT*>(q.y), q.xoff};
+  const int64_t rows = q.re - q.rs;
+  if (rows <= 0) return DACSR_OK;
+  const int order = q.order;
+  const bool exact = order != DACSR_ORDER_TREE;
+  Scal s{q.alpha, q.beta, order, 0};
+  const int sms = sm_count();
+  const bool can_bulk = aligned16(a->values) && aligned16(a->colids);
+
+  switch (q.variant) {
+    case DACSR_VARIANT_ROWBLOCK: {
+      const dacsr_plan_t* p = q.plan;
+      if (!p || p->row_start != q.rs || p->row_end != q.re || !p->block_rows) return DACSR_ERR_PLAN;
+      if (p->cap <= 0 || (p->cap & 15) || !can_bulk) return DACSR_ERR_PLAN;
+      // at most cap/long_len + 1 long rows can start inside one chunk
+      s.long_len = std::max<int64_t>(p->long_len, p->cap / (kMaxLong - 2));
+      const int stages = rowblock_stages<VT, CI>(p->cap);
+      const size_t smem = static_cast<size_t>(stages) * p->cap * (sizeof(VT) + sizeof(CI)) + kScratchBytes;
+      auto kern = rowblock_kernel<KIND, RP, CI, VT>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)) != cudaSuccess)
+        return check_launch("rowblock smem attribute");
+      const int threads = kMaxThreads;
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+      per_sm = std::max(1, per_sm);
+      const int64_t grid = std::min<int64_t>(p->nblocks, static_cast<int64_t>(sms) * per_sm);
+      Chunks c{p->block_rows, p->entry_base, p->entry_end, p->nblocks, p->cap, stages};
+      kern<<<static_cast<unsigned>(grid), threads, smem, q.stream>>>(m, s, c);
+      return check_launch("rowblock_kernel");
+    }
+    case DACSR_VARIANT_STAGED: {
+      const int threads = 256;
+      // capacity: 2x the mean entries of a 256-row block, at most 64 KiB
+      // (the reference-named entry points pass nnz = 0: assume 16 per row)
+      const double mean = a->nnz > 0 && a->nrows ? static_cast<double>(a->nnz) / a->nrows : 16.0;
+      int scap = static_cast<int>(std::min(65536.0 / (sizeof(VT) + sizeof(CI)),
+                                           std::max(512.0, 2.0 * mean * threads)));
+      scap &= ~15;
+      if (!can_bulk) scap = 0;
+      s.long_len = std::max<int64_t>(256, static_cast<int64_t>(8 * mean));
+      const size_t smem = static_cast<size_t>(scap) * (sizeof(VT) + sizeof(CI)) + kScratchBytes;
+      auto kern = staged_kernel<KIND, RP, CI, VT>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)) != cudaSuccess)
+        return check_launch("staged smem attribute");
+      const int64_t grid = (rows + threads - 1) / threads;
+      kern<<<static_cast<unsigned>(grid), threads, smem, q.stream>>>(m, s, q.rs, q.re, scap);
+      return check_launch("staged_kernel");
+    }
+    case DACSR_VARIANT_SCALAR: {
+      const int threads = 256;
+      const int64_t grid = std::min<int64_t>((rows + threads - 1) / threads, sms * 16);
+      scalar_kernel<KIND, RP, CI, VT><<<static_cast<unsigned>(grid), threads, 0, q.stream>>>(
+          m, s, q.rs, q.re);
+      return check_launch("scalar_kernel");
+    }
+    case DACSR_VARIANT_VECTOR2:
+    case DACSR_VARIANT_VECTOR4:
+    case DACSR_VARIANT_VECTOR8:
+    case DACSR_VARIANT_VECTOR16:
+    case DACSR_VARIANT_WARP: {
+      (void)exact;  // vector variants always combine lanes with a tree
+      const int threads = 256;
+      const int g = 2 << (q.variant - DACSR_VARIANT_VECTOR2);
+      const int64_t rows_per_cta = threads / g;
+      const int64_t grid = std::min<int64_t>((rows + rows_per_cta - 1) / rows_per_cta, sms * 16);
+      const unsigned gr = static_cast<unsigned>(std::max<int64_t>(grid, 1));
+      switch (g) {
+        case 2: vector_kernel<2, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
+        case 4: vector_kernel<4, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
+        case 8: vector_kernel<8, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
+        case 16: vector_kernel<16, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
+        default: vector_kernel<32, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
+      }
+      return check_launch("vector_kernel");
+    }
+    default:
+      return DACSR_ERR_VARIANT;
+  }
+}
+
+template <int KIND, class RP, class CI>
+int by_values(const dacsr_matrix_t* a, const Req& q) {
+  if (a->values_dtype == DACSR_F64) return launch<KIND, RP, CI, double>(a, q);
+  if (a->values_dtype == DACSR_F32) return launch<KIND, RP, CI, float>(a, q);
+  return DACSR_ERR_DTYPE;
+}
+
+template <int KIND, class RP>
+int by_colids(const dacsr_matrix_t* a, const Req& q) {
+  if constexpr (KIND == DACSR_KIND_DA) {
+    switch (a->colids_dtype) {
+      case DACSR_I8: return by_values<KIND, RP, int8_t>(a, q);
+      case DACSR_I16: return by_values<KIND, RP, int16_t>(a, q);
+      case DACSR_I32: return by_values<KIND, RP, int32_t>(a, q);
+      default: return DACSR_ERR_DTYPE;
+    }
+  } else {
+    switch (a->colids_dtype) {
+      case DACSR_I32: return by_values<KIND, RP, int32_t>(a, q);
+      case DACSR_I64: return by_values<KIND, RP, int64_t>(a, q);
+      default: return DACSR_ERR_DTYPE;
+    }
+  }
+}
+
+template <int KIND>
+int by_rowptr(const dacsr_matrix_t* a, const Req& q) {
+  if (a->rowptr_dtype == DACSR_I32) return by_colids<KIND, int32_t>(a, q);
+  if (a->rowptr_dtype == DACSR_I64) return by_colids<KIND, int64_t>(a, q);
+  return DACSR_ERR_DTYPE;
+}
+
+}  // namespace
+}  // namespace dacsr
+
+using namespace dacsr;
+
+extern "C" {
+
+const char* dacsr_version(void) { return "dacsr_b200 0.1.0 (sm_100a)"; }
+
+const char* dacsr_last_error(void) { return g_last_error; }
+
+int32_t dacsr_select_variant(const dacsr_stats_t* st, int32_t order) {
+  if (!st) return DACSR_VARIANT_SCALAR;
+  if (order == DACSR_ORDER_TREE && st->mean_len >= 48.0) {
+    if (st->mean_len >= 256.0) return DACSR_VARIANT_WARP;
+    return DACSR_VARIANT_VECTOR16;
+  }
+  return DACSR_VARIANT_ROWBLOCK;
+}
+
+int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t variant, int32_t order,
+               const void* x, int64_t x_offset, void* y, double alpha, double beta,
+               int64_t row_start, int64_t row_end, void* stream) {
+  if (!a || !y || row_start < 0 || row_end < row_start || row_end > a->nrows) return DACSR_ERR_ARG;
+  if (row_end == row_start) return DACSR_OK;
+  if (!a->rowptr || (a->nnz > 0 && (!a->colids || !a->values || !x))) return DACSR_ERR_ARG;
+  if (order < DACSR_ORDER_NAIVE || order > DACSR_ORDER_TREE) return DACSR_ERR_VARIANT;
+  if (variant == DACSR_VARIANT_AUTO) variant = plan ? DACSR_VARIANT_ROWBLOCK : DACSR_VARIANT_STAGED;
+  Req q{plan, variant, order, x, x_offset, y, alpha, beta, row_start, row_end,
+        static_cast<cudaStream_t>(stream)};
+  if (a->kind == DACSR_KIND_DA) return by_rowptr<DACSR_KIND_DA>(a, q);
+  if (a->kind == DACSR_KIND_CSR) return by_rowptr<DACSR_KIND_CSR>(a, q);
+  return DACSR_ERR_DTYPE;
+}
+
+// Reference-named kernels: the paper's layout (int32 rowptr; DA int16
+// offsets, CSR int32 colids), the named order, STAGED engine (no plan).
+#define DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, NAME, ORDER, VT, VCODE, VN)                 \
+  int dacsr_##KIND##_##NAME##_##VN(const int32_t* rowptr, const CI* colids, const VT* values,   \
+                                   const VT* x, VT* y, double alpha, double beta,               \
+                                   int64_t row_start, int64_t row_end, void* stream) {          \
+    dacsr_matrix_t a{KCODE, DACSR_I32, CICODE, VCODE, row_end, 0, 0, rowptr, colids, values};  \
+    return dacsr_spmv(&a, nullptr, DACSR_VARIANT_STAGED, ORDER, x, 0, y, alpha, beta,           \
+                      row_start, row_end, stream);                                              \
+  }
+#define DACSR_DEFINE_KIND(KIND, KCODE, CI, CICODE)                                                  \
+  DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, naive, DACSR_ORDER_NAIVE, double, DACSR_F64, f64)     \
+  DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, shifted_base, DACSR_ORDER_NAIVE, double, DACSR_F64, f64) \
+  DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, multi_acc3, DACSR_ORDER_MACC3, double, DACSR_F64, f64) \
+  DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, strip_mined4, DACSR_ORDER_STRIP4, double, DACSR_F64, f64) \
+  DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, naive, DACSR_ORDER_NAIVE, float, DACSR_F32, f32)      \
+  DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, shifted_base, DACSR_ORDER_NAIVE, float, DACSR_F32, f32) \
+  DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, multi_acc3, DACSR_ORDER_MACC3, float, DACSR_F32, f32) \
+  DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, strip_mined4, DACSR_ORDER_STRIP4, float, DACSR_F32, f32)
+DACSR_DEFINE_KIND(csr, DACSR_KIND_CSR, int32_t, DACSR_I32)
+DACSR_DEFINE_KIND(da, DACSR_KIND_DA, int16_t, DACSR_I16)
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+"""Device-resident matrices: HBM layout, row statistics and the row-block plan.
+
+A ``DeviceMatrix`` owns the three arrays in HBM (torch tensors used only as
+allocations), a ``dacsr_matrix_t`` descriptor for the C ABI, the row-length
+statistics from ``dacsr_analyze`` and the nnz-balanced ROWBLOCK plan
+(block table in HBM).  Layout rules:
+
+* rowptr  int32 when nnz < 2^31, else int64 (C5 on one GPU); narrower host
+  widths (int8/int16, reference test_spmv.py:238-247) widen to int32.
+* inner   DA: int8/int16/int32 offsets kept as given (int16 is the paper's
+  case, 2 bytes/entry); CSR: int32 (int64 only when ncols > 2^31).
+* values  float32/float64 as given.
+All arrays are unpadded and 16-byte aligned (torch allocations are 512-byte
+aligned), which the TMA bulk copies require; kernels never read past nnz.
+
+Host matrices cache their upload (they are immutable), so the reference-
+style ``spmv(A, x, y)`` pays the operator transfer once.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .core import CsrMatrix, DacsrMatrix
+
+_KIND_NAME = {_native.KIND_CSR: "csr", _native.KIND_DA: "da"}
+
+
+def _torch_device(device):
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise ValueError(f"DeviceMatrix needs a CUDA device, got {device}")
+    return device
+
+
+def _upload(arr, dtype, device):
+    a = np.ascontiguousarray(arr, dtype=dtype)
+    if not a.flags.writeable:
+        a = a.copy()
+    return torch.from_numpy(a).to(device)
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class DeviceMatrix:
+    """CSR or DA-CSR matrix in HBM plus its analysis and ROWBLOCK plan."""
+
+    def __init__(self, kind, nrows, ncols, rowptr, colids, values, *, plan=True,
+                 row_start=0, row_end=None, cap=None, long_len=None):
+        if kind not in ("csr", "da"):
+            raise ValueError(f"kind must be 'csr' or 'da', got {kind!r}")
+        for t in (rowptr, colids, values):
+            if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or not t.is_contiguous():
+                raise ValueError("rowptr/colids/values must be contiguous CUDA tensors")
+        self.kind = kind
+        self.nrows, self.ncols = int(nrows), int(ncols)
+        self.rowptr, self.colids, self.values = rowptr, colids, values
+        self.nnz = int(colids.numel())
+        self.device = values.device
+        self.desc = _native.Matrix(
+            _native.KIND_DA if kind == "da" else _native.KIND_CSR,
+            _native.dtype_code(rowptr.dtype), _native.dtype_code(colids.dtype),
+            _native.dtype_code(values.dtype), self.nrows, self.ncols, self.nnz,
+            rowptr.data_ptr(), colids.data_ptr() if self.nnz else None,
+            values.data_ptr() if self.nnz else None)
+        self.row_start = int(row_start)
+        self.row_end = self.nrows if row_end is None else int(row_end)
+        self.stats = None
+        self.plan = None
+        self._block_rows = None
+        self._staging = {}
+        if plan:
+            self.build_plan(cap=cap, long_len=long_len)
+
+    # ---- construction -------------------------------------------------
+    @classmethod
+    def from_host(cls, a, device=None, **kw):
+        """Upload a host CsrMatrix/DacsrMatrix (widening narrow widths)."""
+        device = _torch_device(device)
+        if isinstance(a, DacsrMatrix):
+            kind = "da"
+            inner = a.colids.dtype if a.colids.dtype in (np.int8, np.int16, np.int32) else np.int32
+        elif isinstance(a, CsrMatrix):
+            kind = "csr"
+            inner = np.int64 if a.ncols - 1 > np.iinfo(np.int32).max else np.int32
+        else:
+            raise TypeError(f"expected CsrMatrix or DacsrMatrix, got {type(a).__name__}")
+        rp_dtype = np.int64 if a.nnz > np.iinfo(np.int32).max else np.int32
+        with torch.cuda.device(device):
+            rp = _upload(a.rowptr, rp_dtype, device)
+            ci = _upload(a.colids, inner, device)
+            va = _upload(a.values, a.values.dtype, device)
+            return cls(kind, a.nrows, a.ncols, rp, ci, va, **kw)
+
+    @classmethod
+    def of(cls, a, device=None):
+        """Cached device copy of an (immutable) host matrix."""
+        if isinstance(a, DeviceMatrix):
+            return a
+        device = _torch_device(device)
+        cache = a._device_cache()
+        key = (device.type, device.index)
+        dm = cache.get(key)
+        if dm is None:
+            dm = cls.from_host(a, device)
+            cache[key] = dm
+        return dm
+
+    # ---- analysis and plan -------------------------------------------------
+    def analyze(self, stream=None):
+        st = _native.Stats()
+        scratch = torch.empty(_native.ANALYZE_SCRATCH, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            _native.check(_native.lib().dacsr_analyze(
+                ctypes.byref(self.desc), self.row_start, self.row_end,
+                ctypes.c_void_p(scratch.data_ptr()), ctypes.byref(st), _stream_ptr(stream)),
+                "dacsr_analyze")
+        self.stats = st
+        return st
+
+    def build_plan(self, cap=None, long_len=None, stream=None):
+        L = _native.lib()
+        st = self.stats or self.analyze(stream)
+        if cap is None:
+            cap = L.dacsr_plan_default_cap(ctypes.byref(st), self.desc.values_dtype,
+                                           self.desc.colids_dtype)
+        if long_len is None:
+            long_len = int(max(128, 16 * np.ceil(max(st.mean_len, 1.0))))
+        nb = L.dacsr_plan_nblocks(ctypes.byref(self.desc), st.entry_start, st.entry_end, cap)
+        self._block_rows = torch.empty(nb + 1, dtype=torch.int64, device=self.device)
+        plan = _native.Plan()
+        with torch.cuda.device(self.device):
+            _native.check(L.dacsr_plan_build(
+                ctypes.byref(self.desc), self.row_start, self.row_end, st.entry_start,
+                st.entry_end, int(cap), int(long_len),
+                ctypes.c_void_p(self._block_rows.data_ptr()), ctypes.byref(plan),
+                _stream_ptr(stream)), "dacsr_plan_build")
+        self.plan = plan
+        return plan
+
+    # ---- properties -----------------------------------------------------------
+    @property
+    def iindex_width(self):
+        return self.colids.element_size() * 8
+
+    @property
+    def oindex_width(self):
+        return self.rowptr.element_size() * 8
+
+    @property
+    def scalar_width(self):
+        return self.values.element_size() * 8
+
+    @property
+    def dtype(self):
+        return self.values.dtype
+
+    def storage_bytes(self):
+        return sum(t.numel() * t.element_size() for t in (self.rowptr, self.colids, self.values))
+
+    # ---- the multiply ---------------------------------------------------------
+    def spmv_into(self, x, y, alpha=1.0, beta=0.0, variant="rowblock", order=0, x_offset=0,
+                  row_start=None, row_end=None, stream=None):
+        """Launch y = alpha*A@x + beta*y on device tensors (no validation
+        beyond the C ABI's; ``spmv`` is the validating entry point)."""
+        code = _native.VARIANT_CODES[variant] if isinstance(variant, str) else int(variant)
+        rs = self.row_start if row_start is None else int(row_start)
+        re = self.row_end if row_end is None else int(row_end)
+        plan = self.plan if (self.plan is not None and rs == self.plan.row_start
+                             and re == self.plan.row_end) else None
+        _native.check(_native.lib().dacsr_spmv(
+            ctypes.byref(self.desc), ctypes.byref(plan) if plan is not None else None, code,
+            int(order), ctypes.c_void_p(x.data_ptr()) if x is not None else None, int(x_offset),
+            ctypes.c_void_p(y.data_ptr()), float(alpha), float(beta), rs, re,
+            _stream_ptr(stream)), "dacsr_spmv")
+        return y
+
+    def __repr__(self):
+        return (f"DeviceMatrix({self.kind}, {self.nrows}x{self.ncols}, nnz={self.nnz}, "
+                f"rowptr={self.rowptr.dtype}, inner={self.colids.dtype}, "
+                f"values={self.values.dtype}, device={self.device})")
+
+
+def bandwidth_device(dm, stream=None):
+    """max |col - row| of a DeviceMatrix, computed in HBM."""
+    out = torch.zeros(1, dtype=torch.int64, device=dm.device)
+    with torch.cuda.device(dm.device):
+        _native.check(_native.lib().dacsr_bandwidth(ctypes.byref(dm.desc),
+                                                    ctypes.c_void_p(out.data_ptr()),
+                                                    _stream_ptr(stream)), "dacsr_bandwidth")
+    return int(out.item())
+
+
+def to_dacsr_device(dm, iindex=16, stream=None):
+    """Device-side CSR → DA-CSR (reference core.py:334-355) with the same
+    int-k fit check; rowptr and values are shared, offsets are new."""
+    from .core import index_max
+    from .errors import BandwidthExceedsIndexRange
+    if dm.kind != "csr":
+        raise TypeError("to_dacsr_device expects a CSR DeviceMatrix")
+    limit = index_max(iindex)
+    w = bandwidth_device(dm, stream)
+    if w > limit:
+        raise BandwidthExceedsIndexRange(
+            f"bandwidth {w} exceeds the {iindex}-bit signed offset range [-{limit}, {limit}]")
+    tdt = {8: torch.int8, 16: torch.int16, 32: torch.int32}[iindex]
+    off = torch.empty(dm.nnz, dtype=tdt, device=dm.device)
+    with torch.cuda.device(dm.device):
+        _native.check(_native.lib().dacsr_csr_to_da(
+            ctypes.byref(dm.desc), ctypes.c_void_p(off.data_ptr()), _native.dtype_code(tdt),
+            _stream_ptr(stream)), "dacsr_csr_to_da")
+    return DeviceMatrix("da", dm.nrows, dm.ncols, dm.rowptr, off, dm.values,
+                        row_start=dm.row_start, row_end=dm.row_end)
+
+
+__all__ = ["DeviceMatrix", "bandwidth_device", "to_dacsr_device"]

@@ -91,3 +91,89 @@ def scrambled(a, seed=0):
 
 
 __all__ = ["laplacian_2d", "laplacian_3d", "normal_x", "scrambled", "uniform_x"]
+
+
+def add_skew_rows(a, frac=0.01, alpha=1.5, x_m=1.0, cap=4096, band=None, seed=0):
+    """Give ``frac`` of the rows power-law extra entries (config C4).
+
+    Selected rows (``default_rng(seed).choice(n, round(frac*n))``) receive
+    ``min(cap, floor(x_m * Pareto(alpha)))`` extra distinct columns inside
+    ``[r - band, r + band] ∩ [0, ncols)`` (band defaults to the matrix's
+    bandwidth, so the int16 fit is preserved) with N(0, 1) values.
+    Pareto(alpha) with scale x_m is ``x_m * (1 + rng.pareto(alpha))``.
+    """
+    from .core import bandwidth, entry_rows
+    rng = np.random.default_rng(seed)
+    n, m = a.nrows, a.ncols
+    band = bandwidth(a) if band is None else int(band)
+    rows = np.sort(rng.choice(n, size=int(round(frac * n)), replace=False))
+    extra = np.minimum(cap, np.floor(x_m * (1.0 + rng.pareto(alpha, len(rows))))).astype(np.int64)
+    add_r, add_c = [], []
+    rp = a.rowptr.astype(np.int64)
+    for r, k in zip(rows.tolist(), extra.tolist()):
+        lo, hi = max(0, r - band), min(m - 1, r + band)
+        have = a.colids[rp[r]:rp[r + 1]].astype(np.int64)
+        window = np.setdiff1d(np.arange(lo, hi + 1, dtype=np.int64), have, assume_unique=True)
+        k = min(k, len(window))
+        add_r.append(np.full(k, r, dtype=np.int64))
+        add_c.append(np.sort(rng.choice(window, size=k, replace=False)))
+    add_r = np.concatenate(add_r) if add_r else np.zeros(0, np.int64)
+    add_c = np.concatenate(add_c) if add_c else np.zeros(0, np.int64)
+    add_v = rng.standard_normal(len(add_r)).astype(a.values.dtype)
+    r_all = np.concatenate([entry_rows(a.rowptr), add_r])
+    c_all = np.concatenate([a.colids.astype(np.int64), add_c])
+    v_all = np.concatenate([a.values, add_v])
+    order = np.lexsort((c_all, r_all))
+    counts = np.bincount(r_all, minlength=n)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=rowptr[1:])
+    return _trusted(CsrMatrix, n, m, rowptr.astype(a.rowptr.dtype),
+                    c_all[order].astype(a.colids.dtype), v_all[order])
+
+
+def skewed_rcm_laplacian(nx=2048, scramble_seed=4, skew_seed=5, frac=0.01, alpha=1.5,
+                         x_m=1.0, cap=4096):
+    """Config C4: scrambled nx² Laplacian → RCM → Pareto skew rows in band.
+
+    Returns (matrix, info) where info records the seeds, bandwidths and the
+    RCM permutation (new → old) for parity checks.
+    """
+    from .core import bandwidth
+    from .reorder import permute_symmetric, rcm
+    lap = laplacian_2d(nx)
+    mixed, _ = scrambled(lap, seed=scramble_seed)
+    perm = rcm(mixed)
+    ordered = permute_symmetric(mixed, perm)
+    w = bandwidth(ordered)
+    out = add_skew_rows(ordered, frac=frac, alpha=alpha, x_m=x_m, cap=cap, band=w, seed=skew_seed)
+    info = {"nx": nx, "scramble_seed": scramble_seed, "skew_seed": skew_seed, "frac": frac,
+            "alpha": alpha, "x_m": x_m, "cap": cap, "bandwidth_scrambled": bandwidth(mixed),
+            "bandwidth_rcm": w, "perm": perm.perm}
+    return out, info
+
+
+def poisson_cdf(lam, kmax):
+    """P(K <= k) for k = 0..kmax-1 of Poisson(lam), float64 (host-computed
+    table shared by the device generator and its CPU checker)."""
+    import math
+    out = np.empty(kmax, dtype=np.float64)
+    acc = 0.0
+    for k in range(kmax):
+        acc += math.exp(k * math.log(lam) - lam - math.lgamma(k + 1))
+        out[k] = acc
+    return out
+
+
+def normal_table(points=4096):
+    """``points + 1`` quantiles of N(0, 1) at (i + 0.5) / (points + 1)."""
+    from statistics import NormalDist
+    nd = NormalDist()
+    return np.array([nd.inv_cdf((i + 0.5) / (points + 1)) for i in range(points + 1)],
+                    dtype=np.float64)
+
+
+BANDED_CONFIGS = {
+    # name: (n, half bandwidth, lambda, kmax, seed)
+    "c3": (1 << 24, 32767, 16.0, 64, 2023),
+    "c5": (1 << 28, 32767, 8.0, 32, 2028),
+}

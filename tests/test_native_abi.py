@@ -1,0 +1,54 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol the
+public header declares (no device compute is issued here)."""
+
+import ctypes
+import os
+import re
+
+from conftest import ROOT
+from paper_2307_06305_b200 import _native
+
+HEADER = os.path.join(ROOT, "include", "dacsr_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    names = set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(dacsr_\w+)\s*\(", text, flags=re.M))
+    names.discard("dacsr_")
+    return sorted(n for n in names if not n.startswith("dacsr_##")) + _native.typed_kernel_names()
+
+
+def test_header_functions_found():
+    names = declared_functions()
+    assert "dacsr_spmv" in names and "dacsr_host_rcm" in names
+    assert "dacsr_da_naive_f64" in names and len(names) >= 36
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_bindings_cover_header():
+    assert set(declared_functions()) <= set(_native._SIGNATURES)
+
+
+def test_version_and_error_string():
+    L = _native.lib()
+    assert b"sm_100a" in L.dacsr_version()
+    assert L.dacsr_last_error() is not None
+
+
+def test_arg_validation_without_device():
+    """Argument errors are reported before any CUDA call."""
+    L = _native.lib()
+    assert L.dacsr_spmv(None, None, 0, 0, None, 0, None, 1.0, 0.0, 0, 1, None) == 1
+    m = _native.Matrix(1, 2, 1, 5, 4, 4, 5, None, None, None)
+    assert L.dacsr_spmv(ctypes.byref(m), None, 0, 7, None, 0, ctypes.c_void_p(8), 1.0, 0.0, 0, 4,
+                        None) == 1  # null rowptr
+    assert L.dacsr_plan_nblocks(ctypes.byref(m), 3, 100, 32) == 4
+    st = _native.Stats(4, 5, 0, 5, 2, 0, 1.25, 0.3)
+    cap = L.dacsr_plan_default_cap(ctypes.byref(st), _native.F64, _native.I16)
+    assert cap % 16 == 0 and cap >= 512
