@@ -60,7 +60,12 @@ enum {
   DACSR_VARIANT_VECTOR8 = 5,
   DACSR_VARIANT_VECTOR16 = 6,
   DACSR_VARIANT_WARP = 7,
-  DACSR_VARIANT_STAGED = 8    /* fixed rows per CTA, TMA-bulk staged (no plan)   */
+  DACSR_VARIANT_STAGED = 8,   /* fixed rows per CTA, TMA-bulk staged (no plan)   */
+  DACSR_VARIANT_WSTREAM = 9,  /* warp streams: 32 rows/warp chunk, 128-bit loads */
+                              /* double-buffered in registers, exact orders;     */
+                              /* 256 / 512 / 1024-entry staging windows          */
+  DACSR_VARIANT_WSTREAM512 = 10,
+  DACSR_VARIANT_WSTREAM1024 = 11
 };
 
 /* A matrix in CSR (absolute colids) or DA-CSR (colids = col - row) layout.

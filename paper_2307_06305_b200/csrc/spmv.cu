@@ -321,6 +321,167 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------- WSTREAM (warp streams)
+// Each warp owns chunks of 32 consecutive rows (one per lane), chunk c =
+// gw, gw + W, ... (persistent grid).  The chunk's entries [A, A + VCAP)
+// (A = first entry rounded down to 16 bytes of both arrays) are moved into a
+// warp-private shared-memory slot by the TMA bulk-copy engine: lane 0 issues
+// one cp.async.bulk per array, completion is tracked by a per-slot mbarrier
+// (expect_tx).  Two slots per warp: the copy of the warp's next chunk is in
+// flight while the lanes reduce the current one — no registers spent on
+// staging, no CTA-wide barrier, warps pipeline independently.  Rows are
+// reduced one lane per row in the exact reference order; entries past the
+// staged window come from global; rows longer than long_len are reduced by
+// the whole warp after the others.
+template <class RP, class CI, class VT, int VCAP>
+struct WarpChunk {
+  static constexpr int kVB = VCAP * static_cast<int>(sizeof(VT));  // value bytes per slot
+  static constexpr int kIB = VCAP * static_cast<int>(sizeof(CI));  // index bytes per slot
+  static constexpr int kSlots = 2;
+  static constexpr int kSlot = kVB + ((kIB + 15) & ~15);          // bytes per slot
+  static constexpr int kWarp = kSlots * kSlot;                      // bytes per warp
+  // entries per 16-byte vector of the narrower array: window alignment
+  static constexpr int kAlign = 16 / (sizeof(VT) < sizeof(CI) ? sizeof(VT) : sizeof(CI));
+};
+
+// One row reduced by a whole warp (exact: lane 0 folds in order; TREE: shfl).
+template <int KIND, class RP, class CI, class VT>
+__device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s, int64_t r,
+                                           int64_t b, int64_t e, const VT* sv, const CI* si,
+                                           int64_t A, int64_t H, int lane) {
+  auto get = [&](int64_t i) -> double {
+    if (i < H) {
+      const int k = static_cast<int>(i - A);
+      return product(sv[k], ldg(m.x + m.col(r, si[k])));
+    }
+    return m.prod_global(r, i);
+  };
+  if (s.order == DACSR_ORDER_TREE) {
+    double part = 0.0;
+    for (int64_t i = b + lane; i < e; i += 32) part = __dadd_rn(part, get(i));
+    for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+    if (lane == 0) epilogue(m.y, r, part, s.alpha, s.beta);
+    return;
+  }
+  OrderedAcc acc;
+  acc.init(s.order, e - b);
+  for (int64_t base = b; base < e; base += 32) {
+    const int64_t i = base + lane;
+    const double p = i < e ? get(i) : 0.0;
+    const int n = static_cast<int>(min64(32, e - base));
+    for (int k = 0; k < n; ++k) {
+      const double q = __shfl_sync(0xffffffffu, p, k);
+      if (lane == 0) acc.add(base - b + k, q);
+    }
+  }
+  if (lane == 0) epilogue(m.y, r, acc.result(), s.alpha, s.beta);
+}
+
+template <int KIND, class RP, class CI, class VT, int VCAP>
+__global__ void __launch_bounds__(256, 4)
+    wstream_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re, int64_t nnz) {
+  using WC = WarpChunk<RP, CI, VT, VCAP>;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[8][WC::kSlots];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char* wbase = dsm + wib * WC::kWarp;
+  uint64_t* bar = bars[wib];
+  const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib;
+  const int64_t nchunks = (re - rs + 31) >> 5;
+  if (gw >= nchunks) return;
+  const int64_t last_aligned = (nnz / WC::kAlign) * WC::kAlign;  // bulk copies stay below
+
+  if (lane == 0) {
+    for (int k = 0; k < WC::kSlots; ++k) mbar_init(&bar[k], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+
+  auto window = [&](RP first) -> int64_t {
+    const int64_t f = static_cast<int64_t>(first);
+    return f - (f % WC::kAlign);
+  };
+  // staged entries of a window start A: [A, H)
+  auto limit = [&](int64_t A) { return min64(A + VCAP, last_aligned); };
+  auto issue = [&](int slot, int64_t A) {  // lane 0 only
+    const int64_t H = limit(A);
+    if (H > A) {
+      const uint32_t n = static_cast<uint32_t>(H - A);
+      unsigned char* dst = wbase + slot * WC::kSlot;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bar[slot], n * static_cast<uint32_t>(sizeof(VT) + sizeof(CI)));
+      bulk_copy_g2s(dst, m.v + A, n * sizeof(VT), &bar[slot]);
+      bulk_copy_g2s(dst + WC::kVB, m.ci + A, ((n * sizeof(CI)) + 15) & ~15u, &bar[slot]);
+    }
+  };
+  // row bounds of chunk c: lane l holds the end of row rs+32c+l (clamped)
+  auto rp_end = [&](int64_t c) { return ldg(m.rp + min64(rs + 32 * c + lane + 1, re)); };
+  auto rp_first = [&](int64_t c) { return ldg(m.rp + rs + 32 * c); };
+
+  int64_t c = gw;
+  RP e0 = rp_end(c), f0 = rp_first(c);
+  int64_t A0 = window(f0);
+  if (lane == 0) issue(0, A0);
+  RP e1 = 0, f1 = 0;
+  if (c + W < nchunks) {
+    e1 = rp_end(c + W);
+    f1 = rp_first(c + W);
+  }
+  uint32_t phase = 0;  // bit k = parity of slot k's next completion
+  for (int j = 0; c < nchunks; c += W, ++j) {
+    const int slot = j & 1;
+    const int64_t cn = c + W, cnn = c + 2 * W;
+    // 1. next chunk's copy into the other slot (freed by the last __syncwarp)
+    int64_t A1 = 0;
+    if (cn < nchunks) {
+      A1 = window(f1);
+      if (lane == 0) issue(slot ^ 1, A1);
+    }
+    RP e2 = 0, f2 = 0;
+    if (cnn < nchunks) {
+      e2 = rp_end(cnn);
+      f2 = rp_first(cnn);
+    }
+    // 2. wait for this chunk's bytes
+    const int64_t H = limit(A0);
+    if (H > A0) {
+      mbar_wait(&bar[slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+    }
+    const VT* sv = reinterpret_cast<const VT*>(wbase + slot * WC::kSlot);
+    const CI* si = reinterpret_cast<const CI*>(wbase + slot * WC::kSlot + WC::kVB);
+    // 3. reduce this chunk's rows, one lane per row
+    const int64_t r = rs + 32 * c + lane;
+    int64_t b = __shfl_up_sync(0xffffffffu, static_cast<int64_t>(e0), 1);
+    if (lane == 0) b = f0;
+    const int64_t e = r < re ? static_cast<int64_t>(e0) : b;
+    const bool is_long = (e - b) > s.long_len;
+    if (r < re && !is_long) {
+      auto get = [&](int64_t i) -> double {
+        if (i < H) {
+          const int k = static_cast<int>(i - A0);
+          return product(sv[k], ldg(m.x + m.col(r, si[k])));
+        }
+        return m.prod_global(r, i);
+      };
+      epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
+    }
+    unsigned longs = __ballot_sync(0xffffffffu, r < re && is_long);
+    while (longs) {
+      const int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const int64_t lb = __shfl_sync(0xffffffffu, b, src), le = __shfl_sync(0xffffffffu, e, src);
+      warp_long_row(m, s, rs + 32 * c + src, lb, le, sv, si, A0, H, lane);
+    }
+    __syncwarp();
+    // 4. rotate the pipeline
+    e0 = e1; f0 = f1; A0 = A1;
+    e1 = e2; f1 = f2;
+  }
+}
+
 // ============================================================ host side
 namespace {
 
@@ -441,6 +602,30 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       }
       return check_launch("vector_kernel");
     }
+    case DACSR_VARIANT_WSTREAM:
+    case DACSR_VARIANT_WSTREAM512:
+    case DACSR_VARIANT_WSTREAM1024: {
+      if (!can_bulk) return launch<KIND, RP, CI, VT>(a, Req{q.plan, DACSR_VARIANT_SCALAR, q.order, q.x, q.xoff, q.y, q.alpha, q.beta, q.rs, q.re, q.stream});
+      int vcap = q.variant == DACSR_VARIANT_WSTREAM ? 256 : (q.variant == DACSR_VARIANT_WSTREAM512 ? 512 : 1024);
+      s.long_len = q.plan ? q.plan->long_len : std::max<int64_t>(128, vcap / 4);
+      const int threads = 256;
+      auto go = [&](auto kern, int per_warp) -> int {
+        const size_t smem = static_cast<size_t>(per_warp) * (threads / 32);
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)) != cudaSuccess)
+          return check_launch("wstream smem attribute");
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+        per_sm = std::max(1, per_sm);
+        const int64_t chunks = (rows + 31) / 32;
+        const int64_t grid = std::min<int64_t>((chunks + 7) / 8, static_cast<int64_t>(sms) * per_sm);
+        kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), threads, smem, q.stream>>>(m, s, q.rs, q.re, a->nnz);
+        return check_launch("wstream_kernel");
+      };
+      if (vcap == 256) return go(wstream_kernel<KIND, RP, CI, VT, 256>, WarpChunk<RP, CI, VT, 256>::kWarp);
+      if (vcap == 512) return go(wstream_kernel<KIND, RP, CI, VT, 512>, WarpChunk<RP, CI, VT, 512>::kWarp);
+      return go(wstream_kernel<KIND, RP, CI, VT, 1024>, WarpChunk<RP, CI, VT, 1024>::kWarp);
+    }
     default:
       return DACSR_ERR_VARIANT;
   }
@@ -490,11 +675,14 @@ const char* dacsr_version(void) { return "dacsr_b200 0.1.0 (sm_100a)"; }
 const char* dacsr_last_error(void) { return g_last_error; }
 
 int32_t dacsr_select_variant(const dacsr_stats_t* st, int32_t order) {
-  if (!st) return DACSR_VARIANT_SCALAR;
-  if (order == DACSR_ORDER_TREE && st->mean_len >= 48.0) {
-    if (st->mean_len >= 256.0) return DACSR_VARIANT_WARP;
-    return DACSR_VARIANT_VECTOR16;
-  }
+  if (!st) return DACSR_VARIANT_STAGED;
+  if (order == DACSR_ORDER_TREE && st->mean_len >= 48.0)
+    return st->mean_len >= 256.0 ? DACSR_VARIANT_WARP : DACSR_VARIANT_VECTOR16;
+  // warp streams: a 32-row chunk should fit its staging window ~85% of the time
+  const double chunk = 32.0 * st->mean_len;
+  if (chunk <= 0.85 * 256) return DACSR_VARIANT_WSTREAM;
+  if (chunk <= 0.85 * 512) return DACSR_VARIANT_WSTREAM512;
+  if (chunk <= 0.85 * 1024) return DACSR_VARIANT_WSTREAM1024;
   return DACSR_VARIANT_ROWBLOCK;
 }
 

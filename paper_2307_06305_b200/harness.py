@@ -1,0 +1,133 @@
+"""GPU timing harness in the reference's methodology.
+
+``time_kernel`` follows /root/reference/pkg/src/dacsr/bench.py:96-115
+(warm-up, then epochs that each repeat until both a minimum iteration count
+and a minimum time are met; the result is the minimum per-iteration time)
+but times on the device with CUDA events on the launching stream, with a
+synchronize on both sides.  ``flush_l2`` writes a buffer twice the size of
+the L2 so a measurement can start cold.
+"""
+
+import math
+import subprocess
+import threading
+import time
+
+import torch
+
+_flush_buf = {}
+
+
+def l2_bytes(device=None):
+    props = torch.cuda.get_device_properties(device or torch.cuda.current_device())
+    return int(getattr(props, "L2_cache_size", 126 << 20) or (126 << 20))
+
+
+def flush_l2(device=None, stream=None):
+    """Overwrite 2x L2 worth of memory (evicts every matrix/vector line)."""
+    device = torch.device(device or "cuda")
+    buf = _flush_buf.get(device)
+    if buf is None:
+        buf = torch.empty(2 * l2_bytes(device) // 4, dtype=torch.int32, device=device)
+        _flush_buf[device] = buf
+    with torch.cuda.stream(stream or torch.cuda.current_stream(device)):
+        buf.fill_(1)
+
+
+def time_kernel(fn, epochs=11, warmup_iters=10, min_epoch_iters=10, min_epoch_time=0.1,
+                stream=None, cold=False):
+    """Best-of-epochs per-iteration seconds of ``fn`` measured with CUDA events.
+
+    With ``cold=True`` every iteration is timed individually after an L2
+    flush (the flush is outside the events) and the epoch time is the sum of
+    the per-iteration event times.
+    """
+    stream = stream or torch.cuda.current_stream()
+    for _ in range(warmup_iters):
+        fn()
+    torch.cuda.synchronize()
+    best = math.inf
+    for _ in range(epochs):
+        iters, elapsed = 0, 0.0
+        if cold:
+            while iters < min_epoch_iters or elapsed < min_epoch_time:
+                flush_l2(stream=stream)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                e1.synchronize()
+                elapsed += e0.elapsed_time(e1) / 1e3
+                iters += 1
+        else:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            batch = max(1, min_epoch_iters)
+            e0.record(stream)
+            t0 = time.perf_counter()
+            while True:
+                for _ in range(batch):
+                    fn()
+                iters += batch
+                if time.perf_counter() - t0 >= min_epoch_time or iters >= 1_000_000:
+                    break
+            e1.record(stream)
+            e1.synchronize()
+            elapsed = e0.elapsed_time(e1) / 1e3
+        best = min(best, elapsed / iters)
+    return best
+
+
+class ClockSampler:
+    """Samples nvidia-smi clocks / throttle reasons while running."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0, period_ms=100):
+        self.index = index
+        self.period_ms = period_ms
+        self.rows = []
+        self._proc = None
+        self._thread = None
+
+    def __enter__(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", f"-lms={self.period_ms}"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._thread = threading.Thread(target=self._read, daemon=True)
+            self._thread.start()
+        except OSError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+            self._thread.join(timeout=5)
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[4 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}

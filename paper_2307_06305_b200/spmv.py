@@ -39,15 +39,18 @@ ENV_FLAG = "DACSR_BACKEND"
 
 SERIAL_VARIANTS = ("naive", "shifted_base", "multi_accumulator_3", "strip_mined_4")
 
-# reference variant -> (kernel variant, summation order)
+# reference variant -> (kernel variant, summation order); "exact" is resolved
+# per matrix by the library's selection policy (dacsr_select_variant)
 _EXACT = {
-    "naive": ("rowblock", _native.ORDER_NAIVE),
-    "shifted_base": ("rowblock", _native.ORDER_NAIVE),
-    "multi_accumulator_3": ("rowblock", _native.ORDER_MACC3),
-    "strip_mined_4": ("rowblock", _native.ORDER_STRIP4),
+    "naive": ("exact", _native.ORDER_NAIVE),
+    "shifted_base": ("exact", _native.ORDER_NAIVE),
+    "multi_accumulator_3": ("exact", _native.ORDER_MACC3),
+    "strip_mined_4": ("exact", _native.ORDER_STRIP4),
 }
-GPU_VARIANTS = ("auto", "rowblock", "rowblock_tree", "staged", "scalar", "vector2", "vector4",
-                "vector8", "vector16", "warp")
+_EXACT_KERNELS = ("rowblock", "staged", "scalar", "wstream", "wstream512", "wstream1024")
+_TREE_KERNELS = ("vector2", "vector4", "vector8", "vector16", "warp")
+GPU_VARIANTS = ("auto", "rowblock_tree") + _EXACT_KERNELS + _TREE_KERNELS
+_CODE_NAME = {v: k for k, v in _native.VARIANT_CODES.items()}
 
 
 def available_backends():
@@ -96,7 +99,7 @@ def row_blocks(rowptr, nblocks):
     return list(zip(cuts[:-1], cuts[1:]))
 
 
-def resolve_variant(variant, dm=None):
+def resolve_variant(variant):
     """(kernel variant name, order code) for a user-facing variant."""
     if isinstance(variant, ParallelRowBlock):
         variant = variant.inner
@@ -106,18 +109,25 @@ def resolve_variant(variant, dm=None):
         if variant == "rowblock_tree":
             return "rowblock", _native.ORDER_TREE
         if variant == "auto":
-            if dm is not None and dm.stats is not None:
-                code = _native.lib().dacsr_select_variant(dm.stats, _native.ORDER_NAIVE)
-                name = {v: k for k, v in _native.VARIANT_CODES.items()}[code]
-                return name, _native.ORDER_NAIVE
-            return "rowblock", _native.ORDER_NAIVE
-        if variant in ("rowblock", "staged", "scalar"):
+            return "exact", _native.ORDER_NAIVE
+        if variant in _EXACT_KERNELS:
             return variant, _native.ORDER_NAIVE
-        if variant in ("vector2", "vector4", "vector8", "vector16", "warp"):
+        if variant in _TREE_KERNELS:
             return variant, _native.ORDER_TREE
     raise ValueError(
         f"unknown variant {variant!r}; expected one of {SERIAL_VARIANTS + GPU_VARIANTS} "
         "or a ParallelRowBlock")
+
+
+def kernel_for(dm, kname, order):
+    """Concrete kernel name for a resolved (name, order) on this matrix."""
+    if kname == "exact":
+        if dm.stats is None:
+            return "staged"
+        kname = _CODE_NAME[_native.lib().dacsr_select_variant(dm.stats, order)]
+    if kname == "rowblock" and dm.plan is None:
+        return "staged"
+    return kname
 
 
 def _is_host(v):
@@ -180,10 +190,7 @@ def spmv(a, x, y=None, alpha=1.0, beta=0.0, variant="naive", backend=None, *, st
              torch.empty(nrows, dtype=x.dtype, device=x.device))
 
     dm = DeviceMatrix.of(a, None if not isinstance(x, torch.Tensor) else x.device)
-    if variant == "auto":
-        kname, order = resolve_variant(variant, dm)
-    if kname == "rowblock" and dm.plan is None:
-        kname = "staged"
+    kname = kernel_for(dm, kname, order)
     dev = dm.device
     if isinstance(y, torch.Tensor) and y.device != dev:
         raise ValueError(f"y is on {y.device}, matrix on {dev}")

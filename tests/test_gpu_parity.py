@@ -57,7 +57,8 @@ def test_golden_exact_orders_host_api(cuda, kind, variant):
 
 
 @pytest.mark.parametrize("kind", ["csr", "da"])
-@pytest.mark.parametrize("variant", ["rowblock", "staged", "scalar", "auto"])
+@pytest.mark.parametrize("variant", ["rowblock", "staged", "scalar", "wstream", "wstream512",
+                                     "wstream1024", "auto"])
 def test_golden_exact_kernels_device_api(cuda, kind, variant):
     for k, c in enumerate(CORPUS):
         dm = DeviceMatrix.from_host(host_matrix(c, kind), cuda)
@@ -161,10 +162,16 @@ def test_skewed_long_rows_bit_exact(cuda):
     from paper_2307_06305_b200.workloads import add_skew_rows
     base = laplacian_2d(256)
     a = add_skew_rows(base, frac=0.01, alpha=1.5, cap=4096, band=1024, seed=3)
+    # plus a handful of guaranteed long rows (Pareto tails are rare at this n)
+    a = add_skew_rows(a, frac=12 / a.nrows, alpha=0.05, cap=2000, band=1024, seed=4)
     assert np.diff(a.rowptr).max() > 1000
     x = uniform_x(a.ncols, seed=4)
     _full_parity(a, x)
     _full_parity(dg.to_dacsr(a, 16), x)
+    for kernel in ("rowblock", "staged", "wstream", "wstream512"):
+        y = dg.spmv(dg.to_dacsr(a, 16), x, variant=kernel)
+        ref = oracle.spmv("da", a.rowptr, dg.to_dacsr(a, 16).colids, a.values, x)
+        assert np.array_equal(y.view(np.uint64), ref.view(np.uint64)), kernel
     for variant in ("rowblock_tree", "vector8", "warp"):
         y = dg.spmv(dg.to_dacsr(a, 16), x, variant=variant)
         ref = oracle.spmv("da", a.rowptr, dg.to_dacsr(a, 16).colids, a.values, x)

@@ -73,11 +73,11 @@ def test_backend_env(monkeypatch):
 
 def test_variant_mapping():
     from paper_2307_06305_b200.spmv import resolve_variant
-    assert resolve_variant("naive") == ("rowblock", 0)
-    assert resolve_variant("shifted_base") == ("rowblock", 0)
-    assert resolve_variant("multi_accumulator_3") == ("rowblock", 1)
-    assert resolve_variant("strip_mined_4") == ("rowblock", 2)
-    assert resolve_variant(dg.ParallelRowBlock(8, "strip_mined_4")) == ("rowblock", 2)
+    assert resolve_variant("naive") == ("exact", 0)
+    assert resolve_variant("shifted_base") == ("exact", 0)
+    assert resolve_variant("multi_accumulator_3") == ("exact", 1)
+    assert resolve_variant("strip_mined_4") == ("exact", 2)
+    assert resolve_variant(dg.ParallelRowBlock(8, "strip_mined_4")) == ("exact", 2)
     assert resolve_variant("vector8") == ("vector8", 3)
 
 
