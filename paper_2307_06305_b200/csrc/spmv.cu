@@ -377,36 +377,101 @@ __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s
   if (lane == 0) epilogue(m.y, r, acc.result(), s.alpha, s.beta);
 }
 
-template <int KIND, class RP, class CI, class VT, int VCAP>
+// Fully staged row, exact order, from the warp's smem slot.
+// xr = &x[column base of this row]; all gathers of a batch are issued before
+// the first product is folded.
+template <int ORDER, class CI, class VT>
+__device__ __forceinline__ double staged_dot(const VT* pv, const CI* pi, int n,
+                                             const VT* __restrict__ xr) {
+  if constexpr (ORDER == DACSR_ORDER_NAIVE) {
+    double acc = 0.0;
+    for (int j = 0; j < n; j += 8) {
+      VT xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j + u < n) xv[u] = ldg(xr + pi[j + u]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j + u < n) acc = __dadd_rn(acc, product(pv[j + u], xv[u]));
+    }
+    return acc;
+  } else {
+    auto get = [&](int64_t i) -> double { return product(pv[i], ldg(xr + pi[i])); };
+    return ORDER == DACSR_ORDER_MACC3 ? sum_macc3(0, n, get) : sum_strip4(0, n, get);
+  }
+}
+
+__device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Chunks of 32 rows whose entries [first, last) fit the staging window
+// [A, A + VCAP) with A = first rounded down to 16 bytes ("simple").  The
+// planner lists the others; the hot kernel skips them.
+template <class IT>
+__device__ __forceinline__ bool chunk_fits(IT first, IT last, int vcap, int align, IT last_aligned) {
+  const IT A = first & ~static_cast<IT>(align - 1);
+  IT H = A + vcap;
+  if (H > last_aligned) H = last_aligned;
+  return last <= H;
+}
+
+template <int KIND, class RP, class CI, class VT, int VCAP, int ORDER>
 __global__ void __launch_bounds__(256, 4)
     wstream_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re, int64_t nnz) {
   using WC = WarpChunk<RP, CI, VT, VCAP>;
+  using IT = RP;  // entry positions fit the rowptr type
+  constexpr int kRpSlot = 40;  // rowptr values per slot (33 used)
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[8][WC::kSlots];
+  __shared__ RP rps[8][3][kRpSlot];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   unsigned char* wbase = dsm + wib * WC::kWarp;
   uint64_t* bar = bars[wib];
-  const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib;
-  const int64_t nchunks = (re - rs + 31) >> 5;
+  RP (*rp_slot)[kRpSlot] = rps[wib];
+  const int W = gridDim.x * (blockDim.x >> 5);
+  const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int nchunks = static_cast<int>((re - rs + 31) >> 5);
   if (gw >= nchunks) return;
-  const int64_t last_aligned = (nnz / WC::kAlign) * WC::kAlign;  // bulk copies stay below
+  const IT last_aligned = static_cast<IT>(nnz & ~int64_t(WC::kAlign - 1));
 
   if (lane == 0) {
     for (int k = 0; k < WC::kSlots; ++k) mbar_init(&bar[k], 1);
     mbar_fence_init();
   }
-  __syncwarp();
-
-  auto window = [&](RP first) -> int64_t {
-    const int64_t f = static_cast<int64_t>(first);
-    return f - (f % WC::kAlign);
+  // rowptr slice of chunk c: lane l copies rowptr[rs+32c+l+1] (clamped),
+  // lane 0 also rowptr[rs+32c]
+  auto fetch_rp = [&](int c, int slot) {
+    if (c < nchunks) {
+      const int64_t row0 = rs + 32 * static_cast<int64_t>(c);
+      const RP* src = m.rp + min64(row0 + lane + 1, re);
+      if constexpr (sizeof(RP) == 8) cp_async_8(&rp_slot[slot][lane + 1], src);
+      else cp_async_4(&rp_slot[slot][lane + 1], src);
+      if (lane == 0) {
+        if constexpr (sizeof(RP) == 8) cp_async_8(&rp_slot[slot][0], m.rp + row0);
+        else cp_async_4(&rp_slot[slot][0], m.rp + row0);
+      }
+    }
+    cp_async_commit();
   };
-  // staged entries of a window start A: [A, H)
-  auto limit = [&](int64_t A) { return min64(A + VCAP, last_aligned); };
-  auto issue = [&](int slot, int64_t A) {  // lane 0 only
-    const int64_t H = limit(A);
+  // lane 0: the chunk's entries via the TMA bulk-copy engine
+  auto issue = [&](int slot, IT first) {
+    const IT A = first & ~static_cast<IT>(WC::kAlign - 1);
+    IT H = A + VCAP;
+    if (H > last_aligned) H = last_aligned;
     if (H > A) {
       const uint32_t n = static_cast<uint32_t>(H - A);
       unsigned char* dst = wbase + slot * WC::kSlot;
@@ -416,56 +481,71 @@ __global__ void __launch_bounds__(256, 4)
       bulk_copy_g2s(dst + WC::kVB, m.ci + A, ((n * sizeof(CI)) + 15) & ~15u, &bar[slot]);
     }
   };
-  // row bounds of chunk c: lane l holds the end of row rs+32c+l (clamped)
-  auto rp_end = [&](int64_t c) { return ldg(m.rp + min64(rs + 32 * c + lane + 1, re)); };
-  auto rp_first = [&](int64_t c) { return ldg(m.rp + rs + 32 * c); };
+  auto fits = [&](int slot) {
+    return chunk_fits<IT>(rp_slot[slot][0], rp_slot[slot][32], VCAP, WC::kAlign, last_aligned);
+  };
 
-  int64_t c = gw;
-  RP e0 = rp_end(c), f0 = rp_first(c);
-  int64_t A0 = window(f0);
-  if (lane == 0) issue(0, A0);
-  RP e1 = 0, f1 = 0;
-  if (c + W < nchunks) {
-    e1 = rp_end(c + W);
-    f1 = rp_first(c + W);
+  fetch_rp(gw, 0);
+  fetch_rp(gw + W, 1);
+  cp_async_wait<1>();
+  __syncwarp();
+  if (lane == 0 && fits(0)) issue(0, rp_slot[0][0]);
+  uint32_t phase = 0;
+  int rslot = 0;
+  int k = 0;
+  for (int c = gw; c < nchunks; c += W, ++k) {
+    const int dslot = k & 1;
+    const int rnext = rslot == 2 ? 0 : rslot + 1;
+    const int rnn = rnext == 2 ? 0 : rnext + 1;
+    cp_async_wait<0>();  // rowptr of chunk c + W (issued last iteration)
+    __syncwarp();
+    if (lane == 0 && c + W < nchunks && fits(rnext)) issue(dslot ^ 1, rp_slot[rnext][0]);
+    fetch_rp(c + 2 * W, rnn);
+    if (fits(rslot)) {  // warp-uniform: complex chunks belong to the side kernel
+      const IT first = rp_slot[rslot][0];
+      const IT A = first & ~static_cast<IT>(WC::kAlign - 1);
+      if (rp_slot[rslot][32] > A) {  // non-empty chunk
+        mbar_wait(&bar[dslot], (phase >> dslot) & 1u);
+        phase ^= 1u << dslot;
+      }
+      const int64_t r = rs + 32 * static_cast<int64_t>(c) + lane;
+      if (r < re) {
+        const IT b = rp_slot[rslot][lane], e = rp_slot[rslot][lane + 1];
+        const int kk = static_cast<int>(b - A);
+        const VT* sv = reinterpret_cast<const VT*>(wbase + dslot * WC::kSlot);
+        const CI* si = reinterpret_cast<const CI*>(wbase + dslot * WC::kSlot + WC::kVB);
+        epilogue(m.y, r,
+                 staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b),
+                                   m.x + m.col(r, CI(0))),
+                 s.alpha, s.beta);
+      }
+    }
+    __syncwarp();
+    rslot = rnext;
   }
-  uint32_t phase = 0;  // bit k = parity of slot k's next completion
-  for (int j = 0; c < nchunks; c += W, ++j) {
-    const int slot = j & 1;
-    const int64_t cn = c + W, cnn = c + 2 * W;
-    // 1. next chunk's copy into the other slot (freed by the last __syncwarp)
-    int64_t A1 = 0;
-    if (cn < nchunks) {
-      A1 = window(f1);
-      if (lane == 0) issue(slot ^ 1, A1);
+  cp_async_wait<0>();
+}
+
+// The chunks the planner listed as not fitting the window: one warp per
+// chunk, rows reduced from global in the exact order, long rows by the
+// whole warp.
+template <int KIND, class RP, class CI, class VT>
+__global__ void __launch_bounds__(256)
+    complex_chunks_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re,
+                          const int64_t* __restrict__ chunks, int64_t n_chunks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+       w < n_chunks; w += nw) {
+    const int64_t r = rs + 32 * ldg(chunks + w) + lane;
+    int64_t b = 0, e = 0;
+    if (r < re) {
+      b = ldg(m.rp + r);
+      e = ldg(m.rp + r + 1);
     }
-    RP e2 = 0, f2 = 0;
-    if (cnn < nchunks) {
-      e2 = rp_end(cnn);
-      f2 = rp_first(cnn);
-    }
-    // 2. wait for this chunk's bytes
-    const int64_t H = limit(A0);
-    if (H > A0) {
-      mbar_wait(&bar[slot], (phase >> slot) & 1u);
-      phase ^= 1u << slot;
-    }
-    const VT* sv = reinterpret_cast<const VT*>(wbase + slot * WC::kSlot);
-    const CI* si = reinterpret_cast<const CI*>(wbase + slot * WC::kSlot + WC::kVB);
-    // 3. reduce this chunk's rows, one lane per row
-    const int64_t r = rs + 32 * c + lane;
-    int64_t b = __shfl_up_sync(0xffffffffu, static_cast<int64_t>(e0), 1);
-    if (lane == 0) b = f0;
-    const int64_t e = r < re ? static_cast<int64_t>(e0) : b;
     const bool is_long = (e - b) > s.long_len;
     if (r < re && !is_long) {
-      auto get = [&](int64_t i) -> double {
-        if (i < H) {
-          const int k = static_cast<int>(i - A0);
-          return product(sv[k], ldg(m.x + m.col(r, si[k])));
-        }
-        return m.prod_global(r, i);
-      };
+      auto get = [&](int64_t i) { return m.prod_global(r, i); };
       epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
     }
     unsigned longs = __ballot_sync(0xffffffffu, r < re && is_long);
@@ -473,12 +553,27 @@ __global__ void __launch_bounds__(256, 4)
       const int src = __ffs(longs) - 1;
       longs &= longs - 1;
       const int64_t lb = __shfl_sync(0xffffffffu, b, src), le = __shfl_sync(0xffffffffu, e, src);
-      warp_long_row(m, s, rs + 32 * c + src, lb, le, sv, si, A0, H, lane);
+      warp_long_row(m, s, r - lane + src, lb, le, static_cast<const VT*>(nullptr),
+                    static_cast<const CI*>(nullptr), 0, 0, lane);
     }
-    __syncwarp();
-    // 4. rotate the pipeline
-    e0 = e1; f0 = f1; A0 = A1;
-    e1 = e2; f1 = f2;
+  }
+}
+
+// planner: list the 32-row chunks that do not fit a VCAP window
+template <class RP>
+__global__ void classify_chunks_kernel(const RP* __restrict__ rp, int64_t rs, int64_t re,
+                                       int vcap, int align, int64_t last_aligned,
+                                       int64_t* out, unsigned long long* count) {
+  const int64_t nchunks = (re - rs + 31) >> 5;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < nchunks;
+       c += stride) {
+    const int64_t first = static_cast<int64_t>(rp[rs + 32 * c]);
+    const int64_t last = static_cast<int64_t>(rp[min64(rs + 32 * c + 32, re)]);
+    if (!chunk_fits<int64_t>(first, last, vcap, align, last_aligned)) {
+      const unsigned long long slot = atomicAdd(count, 1ull);
+      out[slot] = c;
+    }
   }
 }
 
@@ -501,6 +596,40 @@ int sm_count() {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Per-kernel launch configuration, computed once per (kernel, smem bytes):
+// the max-dynamic-smem attribute and the occupancy query cost microseconds
+// of host time, which would otherwise sit between back-to-back launches.
+struct LaunchCache {
+  std::mutex mu;
+  const void* fn[64] = {};
+  size_t smem[64] = {};
+  int per_sm[64] = {};
+  int n = 0;
+};
+
+template <class K>
+int cached_per_sm(K kern, int threads, size_t smem) {
+  static LaunchCache cache;
+  const void* key = reinterpret_cast<const void*>(kern);
+  std::lock_guard<std::mutex> lock(cache.mu);
+  for (int i = 0; i < cache.n; ++i)
+    if (cache.fn[i] == key && cache.smem[i] == smem) return cache.per_sm[i];
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return -1;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess)
+    return -1;
+  per_sm = std::max(1, per_sm);
+  if (cache.n < 64) {
+    cache.fn[cache.n] = key;
+    cache.smem[cache.n] = smem;
+    cache.per_sm[cache.n] = per_sm;
+    ++cache.n;
+  }
+  return per_sm;
+}
 
 struct Req {
   const dacsr_plan_t* plan;
@@ -544,13 +673,9 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       const int stages = rowblock_stages<VT, CI>(p->cap);
       const size_t smem = static_cast<size_t>(stages) * p->cap * (sizeof(VT) + sizeof(CI)) + kScratchBytes;
       auto kern = rowblock_kernel<KIND, RP, CI, VT>;
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)) != cudaSuccess)
-        return check_launch("rowblock smem attribute");
       const int threads = kMaxThreads;
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-      per_sm = std::max(1, per_sm);
+      const int per_sm = cached_per_sm(kern, threads, smem);
+      if (per_sm < 0) return check_launch("rowblock launch config");
       const int64_t grid = std::min<int64_t>(p->nblocks, static_cast<int64_t>(sms) * per_sm);
       Chunks c{p->block_rows, p->entry_base, p->entry_end, p->nblocks, p->cap, stages};
       kern<<<static_cast<unsigned>(grid), threads, smem, q.stream>>>(m, s, c);
@@ -568,9 +693,7 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       s.long_len = std::max<int64_t>(256, static_cast<int64_t>(8 * mean));
       const size_t smem = static_cast<size_t>(scap) * (sizeof(VT) + sizeof(CI)) + kScratchBytes;
       auto kern = staged_kernel<KIND, RP, CI, VT>;
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)) != cudaSuccess)
-        return check_launch("staged smem attribute");
+      if (cached_per_sm(kern, threads, smem) < 0) return check_launch("staged launch config");
       const int64_t grid = (rows + threads - 1) / threads;
       kern<<<static_cast<unsigned>(grid), threads, smem, q.stream>>>(m, s, q.rs, q.re, scap);
       return check_launch("staged_kernel");
@@ -605,26 +728,42 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
     case DACSR_VARIANT_WSTREAM:
     case DACSR_VARIANT_WSTREAM512:
     case DACSR_VARIANT_WSTREAM1024: {
-      if (!can_bulk) return launch<KIND, RP, CI, VT>(a, Req{q.plan, DACSR_VARIANT_SCALAR, q.order, q.x, q.xoff, q.y, q.alpha, q.beta, q.rs, q.re, q.stream});
-      int vcap = q.variant == DACSR_VARIANT_WSTREAM ? 256 : (q.variant == DACSR_VARIANT_WSTREAM512 ? 512 : 1024);
-      s.long_len = q.plan ? q.plan->long_len : std::max<int64_t>(128, vcap / 4);
+      const int vcap = q.variant == DACSR_VARIANT_WSTREAM ? 256
+                       : (q.variant == DACSR_VARIANT_WSTREAM512 ? 512 : 1024);
+      const dacsr_plan_t* p = q.plan;
+      if (!p || p->chunk_vcap != vcap || p->row_start != q.rs || p->row_end != q.re ||
+          (p->n_complex > 0 && !p->complex_chunks) || !can_bulk)
+        return DACSR_ERR_PLAN;
+      if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
+        // warp streams specialise the naive order; the others run row blocks
+        Req r2 = q;
+        r2.variant = p->block_rows ? DACSR_VARIANT_ROWBLOCK : DACSR_VARIANT_STAGED;
+        return launch<KIND, RP, CI, VT>(a, r2);
+      }
       const int threads = 256;
       auto go = [&](auto kern, int per_warp) -> int {
         const size_t smem = static_cast<size_t>(per_warp) * (threads / 32);
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)) != cudaSuccess)
-          return check_launch("wstream smem attribute");
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-        per_sm = std::max(1, per_sm);
+        const int per_sm = cached_per_sm(kern, threads, smem);
+        if (per_sm < 0) return check_launch("wstream launch config");
         const int64_t chunks = (rows + 31) / 32;
         const int64_t grid = std::min<int64_t>((chunks + 7) / 8, static_cast<int64_t>(sms) * per_sm);
-        kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), threads, smem, q.stream>>>(m, s, q.rs, q.re, a->nnz);
+        kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), threads, smem, q.stream>>>(
+            m, s, q.rs, q.re, a->nnz);
         return check_launch("wstream_kernel");
       };
-      if (vcap == 256) return go(wstream_kernel<KIND, RP, CI, VT, 256>, WarpChunk<RP, CI, VT, 256>::kWarp);
-      if (vcap == 512) return go(wstream_kernel<KIND, RP, CI, VT, 512>, WarpChunk<RP, CI, VT, 512>::kWarp);
-      return go(wstream_kernel<KIND, RP, CI, VT, 1024>, WarpChunk<RP, CI, VT, 1024>::kWarp);
+      int rc;
+      if (vcap == 256)
+        rc = go(wstream_kernel<KIND, RP, CI, VT, 256, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 256>::kWarp);
+      else if (vcap == 512)
+        rc = go(wstream_kernel<KIND, RP, CI, VT, 512, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 512>::kWarp);
+      else
+        rc = go(wstream_kernel<KIND, RP, CI, VT, 1024, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 1024>::kWarp);
+      if (rc || p->n_complex == 0) return rc;
+      s.long_len = std::max<int64_t>(p->long_len, 32);
+      const int64_t grid = std::min<int64_t>((p->n_complex + 7) / 8, static_cast<int64_t>(sms) * 16);
+      complex_chunks_kernel<KIND, RP, CI, VT><<<static_cast<unsigned>(grid), threads, 0, q.stream>>>(
+          m, s, q.rs, q.re, p->complex_chunks, p->n_complex);
+      return check_launch("complex_chunks_kernel");
     }
     default:
       return DACSR_ERR_VARIANT;
@@ -680,10 +819,56 @@ int32_t dacsr_select_variant(const dacsr_stats_t* st, int32_t order) {
     return st->mean_len >= 256.0 ? DACSR_VARIANT_WARP : DACSR_VARIANT_VECTOR16;
   // warp streams: a 32-row chunk should fit its staging window ~85% of the time
   const double chunk = 32.0 * st->mean_len;
-  if (chunk <= 0.85 * 256) return DACSR_VARIANT_WSTREAM;
-  if (chunk <= 0.85 * 512) return DACSR_VARIANT_WSTREAM512;
-  if (chunk <= 0.85 * 1024) return DACSR_VARIANT_WSTREAM1024;
+  if (chunk <= 0.95 * 256) return DACSR_VARIANT_WSTREAM;
+  if (chunk <= 0.95 * 512) return DACSR_VARIANT_WSTREAM512;
+  if (chunk <= 0.95 * 1024) return DACSR_VARIANT_WSTREAM1024;
   return DACSR_VARIANT_ROWBLOCK;
+}
+
+int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t rs, int64_t re, int32_t vcap,
+                      int64_t* chunks_dev, void* count_scratch_dev, dacsr_plan_t* inout,
+                      void* stream) {
+  if (!a || !inout || !chunks_dev || !count_scratch_dev || rs < 0 || re < rs || re > a->nrows ||
+      (vcap != 256 && vcap != 512 && vcap != 1024))
+    return DACSR_ERR_ARG;
+  static const int kBytes[6] = {1, 2, 4, 8, 4, 8};
+  if (a->values_dtype < 0 || a->values_dtype > 5 || a->colids_dtype < 0 || a->colids_dtype > 5)
+    return DACSR_ERR_DTYPE;
+  const int narrow = std::min(kBytes[a->values_dtype], kBytes[a->colids_dtype]);
+  const int align = 16 / narrow;
+  const int64_t last_aligned = a->nnz & ~static_cast<int64_t>(align - 1);
+  auto st = static_cast<cudaStream_t>(stream);
+  auto* count = static_cast<unsigned long long*>(count_scratch_dev);
+  cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) {
+    set_last_error("plan_chunks memset", e);
+    return DACSR_ERR_CUDA;
+  }
+  const int64_t nchunks = (re - rs + 31) / 32;
+  if (nchunks > 0) {
+    const int g = static_cast<int>(std::min<int64_t>((nchunks + 255) / 256, 148 * 32));
+    if (a->rowptr_dtype == DACSR_I64)
+      classify_chunks_kernel<int64_t><<<g, 256, 0, st>>>(static_cast<const int64_t*>(a->rowptr), rs, re,
+                                                         vcap, align, last_aligned, chunks_dev, count);
+    else if (a->rowptr_dtype == DACSR_I32)
+      classify_chunks_kernel<int32_t><<<g, 256, 0, st>>>(static_cast<const int32_t*>(a->rowptr), rs, re,
+                                                         vcap, align, last_aligned, chunks_dev, count);
+    else
+      return DACSR_ERR_DTYPE;
+    int rc = check_launch("classify_chunks_kernel");
+    if (rc) return rc;
+  }
+  unsigned long long h = 0;
+  e = cudaMemcpyAsync(&h, count, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    set_last_error("plan_chunks count", e);
+    return DACSR_ERR_CUDA;
+  }
+  inout->chunk_vcap = vcap;
+  inout->n_complex = static_cast<int64_t>(h);
+  inout->complex_chunks = chunks_dev;
+  return DACSR_OK;
 }
 
 int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t variant, int32_t order,

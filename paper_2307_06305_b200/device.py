@@ -75,7 +75,7 @@ class DeviceMatrix:
         self.stats = None
         self.plan = None
         self._block_rows = None
-        self._staging = {}
+        self._chunk_plans = {}
         if plan:
             self.build_plan(cap=cap, long_len=long_len)
 
@@ -145,6 +145,40 @@ class DeviceMatrix:
         self.plan = plan
         return plan
 
+    _VCAP = {"wstream": 256, "wstream512": 512, "wstream1024": 1024}
+
+    def chunk_plan(self, vcap, stream=None):
+        """Plan copy carrying the WSTREAM chunk classification for ``vcap``."""
+        got = self._chunk_plans.get(vcap)
+        if got is not None:
+            return got[0]
+        if self.plan is None:
+            self.build_plan(stream=stream)
+        plan = _native.Plan()
+        ctypes.memmove(ctypes.byref(plan), ctypes.byref(self.plan), ctypes.sizeof(plan))
+        nchunks = max(1, (self.row_end - self.row_start + 31) // 32)
+        chunks = torch.empty(nchunks, dtype=torch.int64, device=self.device)
+        count = torch.empty(1, dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            _native.check(_native.lib().dacsr_plan_chunks(
+                ctypes.byref(self.desc), self.row_start, self.row_end, int(vcap),
+                ctypes.c_void_p(chunks.data_ptr()), ctypes.c_void_p(count.data_ptr()),
+                ctypes.byref(plan), _stream_ptr(stream)), "dacsr_plan_chunks")
+        self._chunk_plans[vcap] = (plan, chunks)
+        return plan
+
+    def plan_for(self, kname, row_start=None, row_end=None):
+        """The plan a kernel needs (None when it needs none or the row range
+        differs from the planned one)."""
+        rs = self.row_start if row_start is None else row_start
+        re = self.row_end if row_end is None else row_end
+        if self.plan is None or rs != self.plan.row_start or re != self.plan.row_end:
+            return None
+        vcap = self._VCAP.get(kname)
+        if vcap is not None:
+            return self.chunk_plan(vcap)
+        return self.plan
+
     # ---- properties -----------------------------------------------------------
     @property
     def iindex_width(self):
@@ -173,8 +207,7 @@ class DeviceMatrix:
         code = _native.VARIANT_CODES[variant] if isinstance(variant, str) else int(variant)
         rs = self.row_start if row_start is None else int(row_start)
         re = self.row_end if row_end is None else int(row_end)
-        plan = self.plan if (self.plan is not None and rs == self.plan.row_start
-                             and re == self.plan.row_end) else None
+        plan = self.plan_for(variant if isinstance(variant, str) else "", rs, re)
         _native.check(_native.lib().dacsr_spmv(
             ctypes.byref(self.desc), ctypes.byref(plan) if plan is not None else None, code,
             int(order), ctypes.c_void_p(x.data_ptr()) if x is not None else None, int(x_offset),

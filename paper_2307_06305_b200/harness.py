@@ -34,15 +34,39 @@ def flush_l2(device=None, stream=None):
         buf.fill_(1)
 
 
+class GraphBatch:
+    """``n`` back-to-back calls of ``fn`` captured once in a CUDA graph, so
+    replays carry no host launch overhead between kernels."""
+
+    def __init__(self, fn, n, stream=None):
+        self.n = n
+        fn()  # warm: lazy init, launch-config caches
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        s = stream or torch.cuda.Stream()
+        with torch.cuda.graph(self.graph, stream=s):
+            for _ in range(n):
+                fn()
+        torch.cuda.synchronize()
+
+    def __call__(self):
+        self.graph.replay()
+
+
 def time_kernel(fn, epochs=11, warmup_iters=10, min_epoch_iters=10, min_epoch_time=0.1,
-                stream=None, cold=False):
+                stream=None, cold=False, graph=0):
     """Best-of-epochs per-iteration seconds of ``fn`` measured with CUDA events.
 
     With ``cold=True`` every iteration is timed individually after an L2
     flush (the flush is outside the events) and the epoch time is the sum of
-    the per-iteration event times.
+    the per-iteration event times.  With ``graph=n`` (warm mode) ``fn`` is
+    captured n times into a CUDA graph that is replayed instead.
     """
     stream = stream or torch.cuda.current_stream()
+    per_call = 1
+    if graph and not cold:
+        fn = GraphBatch(fn, graph)
+        per_call = graph
     for _ in range(warmup_iters):
         fn()
     torch.cuda.synchronize()
@@ -75,7 +99,7 @@ def time_kernel(fn, epochs=11, warmup_iters=10, min_epoch_iters=10, min_epoch_ti
             e1.record(stream)
             e1.synchronize()
             elapsed = e0.elapsed_time(e1) / 1e3
-        best = min(best, elapsed / iters)
+        best = min(best, elapsed / (iters * per_call))
     return best
 
 

@@ -125,7 +125,9 @@ def kernel_for(dm, kname, order):
         if dm.stats is None:
             return "staged"
         kname = _CODE_NAME[_native.lib().dacsr_select_variant(dm.stats, order)]
-    if kname == "rowblock" and dm.plan is None:
+    if kname.startswith("wstream") and order in (_native.ORDER_MACC3, _native.ORDER_STRIP4):
+        kname = "rowblock"  # warp streams specialise the naive order
+    if kname in ("rowblock", "wstream", "wstream512", "wstream1024") and dm.plan is None:
         return "staged"
     return kname
 

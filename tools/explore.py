@@ -36,8 +36,8 @@ def run(name, mats, x):
             kname = kernel_for(dm, kname, order)
             fn = lambda: dm.spmv_into(x, y, 1.0, 0.0, kname, order)
             try:
-                t = time_kernel(fn, epochs=5, warmup_iters=5, min_epoch_iters=20,
-                                min_epoch_time=0.05, cold=args.cold)
+                t = time_kernel(fn, epochs=5, warmup_iters=3, min_epoch_iters=3,
+                                min_epoch_time=0.05, cold=args.cold, graph=0 if args.cold else 20)
             except Exception as e:  # noqa
                 print(name, kind, v, "ERROR", e, flush=True)
                 continue
