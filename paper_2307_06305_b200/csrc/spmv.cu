@@ -600,12 +600,16 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // Per-kernel launch configuration, computed once per (kernel, smem bytes):
 // the max-dynamic-smem attribute and the occupancy query cost microseconds
 // of host time, which would otherwise sit between back-to-back launches.
+// The attribute is raised once per kernel to the device's opt-in maximum
+// (it is a cap, not a reservation), so cached entries stay launchable.
 struct LaunchCache {
   std::mutex mu;
-  const void* fn[64] = {};
-  size_t smem[64] = {};
-  int per_sm[64] = {};
+  const void* fn[96] = {};
+  size_t smem[96] = {};
+  int per_sm[96] = {};
   int n = 0;
+  const void* raised[96] = {};
+  int n_raised = 0;
 };
 
 template <class K>
@@ -615,14 +619,25 @@ int cached_per_sm(K kern, int threads, size_t smem) {
   std::lock_guard<std::mutex> lock(cache.mu);
   for (int i = 0; i < cache.n; ++i)
     if (cache.fn[i] == key && cache.smem[i] == smem) return cache.per_sm[i];
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem)) != cudaSuccess)
-    return -1;
+  bool raised = false;
+  for (int i = 0; i < cache.n_raised; ++i) raised |= cache.raised[i] == key;
+  if (!raised) {
+    int dev = 0, optin = 227 * 1024;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return -1;
+    const int dyn_max = optin - static_cast<int>(fa.sharedSizeBytes);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) !=
+        cudaSuccess)
+      return -1;
+    if (cache.n_raised < 96) cache.raised[cache.n_raised++] = key;
+  }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess)
     return -1;
   per_sm = std::max(1, per_sm);
-  if (cache.n < 64) {
+  if (cache.n < 96) {
     cache.fn[cache.n] = key;
     cache.smem[cache.n] = smem;
     cache.per_sm[cache.n] = per_sm;
