@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-suite", action="store_true", help="skip the C1/C2-f32/C3/C4 lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--suite", default="c1,c2f32,c3,c4")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="c2: 100 back-to-back SpMVs (default); c5: 50-iteration power "
+                         "iteration on the 2^28-row banded matrix")
     return ap.parse_args()
 
 
@@ -292,6 +295,63 @@ def suite_builders():
     return {"c1": c1, "c2f32": c2f32, "c3": c3, "c4": c4}
 
 
+def run_c5(args, world, rank, local):
+    """Config C5: 50 normalised power iterations x <- A x / ||A x|| on the
+    2^28-row random banded matrix (b = 32767, Poisson(8) clamped [1, 32]),
+    DA-CSR i16 with int64 rowptr, generated on the device.  One step = the
+    50 iterations (50 SpMVs + 50 deterministic norms)."""
+    import torch
+    from paper_2307_06305_b200.device import DeviceMatrix
+    from paper_2307_06305_b200.gen import banded_arrays, normal_vector
+    from paper_2307_06305_b200.harness import ClockSampler
+    from paper_2307_06305_b200.power import power_iteration
+    from paper_2307_06305_b200.workloads import BANDED_CONFIGS
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n, b, lam, kmax, seed = BANDED_CONFIGS["c5"]
+    t0 = time.time()
+    arr = banded_arrays(n, b, lam, kmax, seed, dev, kinds=("da",))
+    dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"])
+    x0 = normal_vector(n, 21, dev)
+    build_s = time.time() - t0
+    o = dm.oindex_width // 8
+    traffic = traffic_of(n, dm.nnz, o, 2, 8)
+    iters = 50
+    for _ in range(args.warmup):
+        power_iteration(dm, x0, iters=2)
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, norms = power_iteration(dm, x0, iters=iters)
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    step = sum(times) / len(times)
+    peak, peak_src = peaks()
+    line = {
+        "metric": "SpMV effective HBM GB/s (DA-CSR i16, f64)",
+        "value": round(iters * traffic / step / 1e9, 1), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "C5: power iteration, 50 iters, banded n=2^28 b=32767 "
+                               "Poisson(8) in [1,32], DA-CSR i16 + int64 rowptr",
+                   "nnz": dm.nnz, "bytes_per_spmv": traffic, "build_s": round(build_s, 1),
+                   "final_norm": norms[-1]},
+        "roofline": {"bound": "hbm", "achieved": round(iters * traffic / step / 1e9, 1),
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(iters * traffic / step / 1e9 / peak, 4), "traffic": None,
+                     "peak_source": peak_src},
+        "gpu_launches": args.steps * iters * 3,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(args):
     import torch
     import paper_2307_06305_b200 as dg
@@ -301,6 +361,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload == "c5" and world == 1:
+        return run_c5(args, world, rank, local)
     if world > 1:
         from paper_2307_06305_b200 import distributed
         return distributed.bench_main(args, rank, world, local)

@@ -78,10 +78,12 @@ def _rowptr_arg(rowptr):
 
 
 def spmv_kernel(kind, rowptr, colids, values, x, y, alpha, beta, order="naive",
-                row_start=0, row_end=None, threads=1):
+                row_start=0, row_end=None, threads=1, x_offset=0):
     """Run the restated reference kernel in place on ``y``.
 
     ``kind`` is "csr" or "da"; ``threads > 1`` is ParallelRowBlock(threads).
+    ``x_offset`` shifts x addressing (x[col + x_offset]) for rank-local halo
+    buffers; the reference kernel is the x_offset == 0 case.
     """
     rp = _rowptr_arg(rowptr)
     ci = np.ascontiguousarray(colids)
@@ -91,8 +93,9 @@ def spmv_kernel(kind, rowptr, colids, values, x, y, alpha, beta, order="naive",
     nrows = len(rp) - 1
     row_end = nrows if row_end is None else row_end
     k = {"csr": 0, "da": 1}[kind]
+    xp = ctypes.c_void_p((xx.ctypes.data or 0) + int(x_offset) * xx.itemsize)
     args = (k, ORDERS[order], _DT[rp.dtype], _DT[ci.dtype], _DT[v.dtype],
-            _p(rp), _p(ci), _p(v), _p(xx), _p(y), float(alpha), float(beta))
+            _p(rp), _p(ci), _p(v), xp, _p(y), float(alpha), float(beta))
     if threads == 1:
         rc = lib().orc_spmv(*args, row_start, row_end)
     else:
@@ -245,3 +248,38 @@ def gen_normal(seed, i0, i1, table):
     out = np.empty(i1 - i0, np.float64)
     lib().orc_gen_normal(seed, i0, i1, _p(table), _p(out))
     return out
+
+
+# ---- deterministic norm restatement (csrc/aux.cu sumsq_kernel) -----------
+
+def sumsq_chunks(y, chunk):
+    """Per-chunk sum of y^2 in the device kernel's fixed order: 256 lanes
+    each fold y[c0+t::256] left to right, a 5-step xor butterfly per 32
+    lanes, then the 8 warp sums left to right."""
+    y = np.asarray(y, dtype=np.float64)
+    n = len(y)
+    out = []
+    for c0 in range(0, n, chunk):
+        seg = y[c0:min(n, c0 + chunk)]
+        lanes = np.zeros(256)
+        for t in range(256):
+            acc = 0.0
+            for v in seg[t::256].tolist():
+                acc = acc + v * v
+            lanes[t] = acc
+        w = lanes.reshape(8, 32).copy()
+        for o in (16, 8, 4, 2, 1):
+            idx = np.arange(32) ^ o
+            w = w + w[:, idx]
+        t = 0.0
+        for k in range(8):
+            t = t + float(w[k, 0])
+        out.append(t)
+    return np.array(out)
+
+
+def fold_ordered(partials):
+    t = 0.0
+    for v in np.asarray(partials, dtype=np.float64).tolist():
+        t = t + v
+    return t

@@ -1,0 +1,93 @@
+"""Device side of the multi-GPU path on one GPU: the rank-local x_offset /
+row-range kernels, the deterministic norm, and the power iteration, all
+bit-exact against the CPU oracle.  (NCCL ranks cannot share one GPU; the
+exchange logic itself is covered by tests/test_distributed.py on gloo.)"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2307_06305_b200 import distributed as D
+from paper_2307_06305_b200.device import DeviceMatrix
+from paper_2307_06305_b200.gen import banded_arrays, normal_vector
+from paper_2307_06305_b200.power import chunk_partials, fold_ordered, power_iteration
+from paper_2307_06305_b200.workloads import BANDED_CONFIGS, normal_table, poisson_cdf
+
+pytestmark = pytest.mark.gpu
+
+N, B, LAM, KMAX, SEED = 1 << 16, 3000, 8.0, 32, 5
+
+
+def test_sumsq_matches_oracle_restatement(cuda):
+    y = normal_vector(300_001, 3, cuda)
+    p = chunk_partials(y, 4096)
+    want = oracle.sumsq_chunks(y.cpu().numpy(), 4096)
+    assert np.array_equal(p.cpu().numpy().view(np.uint64), want.view(np.uint64))
+    assert float(fold_ordered(p).item()) == oracle.fold_ordered(want)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_rank_local_blocks_bit_exact(cuda, world):
+    arr = banded_arrays(N, B, LAM, KMAX, SEED, cuda, kinds=("da", "csr"))
+    full = DeviceMatrix("da", N, N, arr["rowptr"], arr["offsets"], arr["values"])
+    x = normal_vector(N, 9, cuda)
+    y_full = torch.empty(N, dtype=torch.float64, device=cuda)
+    full.spmv_into(x, y_full, 0.75, 0.0, "wstream")
+    part = D.RowPartition.equal(N, world, align=1024)
+    ys = []
+    for rank in range(world):
+        plan = D.halo_plan(part, rank, B)
+        r0, r1 = part.bounds[rank]
+        loc = banded_arrays(N, B, LAM, KMAX, SEED, cuda, r0=r0, r1=r1, kinds=("da", "csr"))
+        x_ext = x[plan.lo:plan.hi].clone()        # what the halo exchange delivers
+        for kind, inner in (("da", "offsets"), ("csr", "colids")):
+            op = D.CudaLocalOp(kind, loc["rowptr"], loc[inner], loc["values"], N, plan, 1024, B)
+            y = torch.empty(r1 - r0, dtype=torch.float64, device=cuda)
+            for which in range(3):
+                op.spmv_part(which, x_ext, y, 0.75)
+            if kind == "da":
+                ys.append(y)
+            else:
+                assert torch.equal(y, ys[-1])
+    assert torch.equal(torch.cat(ys), y_full)
+
+
+def test_power_iteration_matches_oracle(cuda):
+    arr = banded_arrays(N, B, LAM, KMAX, SEED, cuda)
+    dm = DeviceMatrix("da", N, N, arr["rowptr"], arr["offsets"], arr["values"])
+    x0 = normal_vector(N, 11, cuda)
+    x, norms = power_iteration(dm, x0, iters=8, chunk=4096)
+    rp, offs, vals = oracle.gen_fill(N, B, KMAX, SEED, poisson_cdf(LAM, KMAX), normal_table())
+    xr = x0.cpu().numpy()
+    s = np.sqrt(oracle.fold_ordered(oracle.sumsq_chunks(xr, 4096)))
+    for k in range(8):
+        xr = oracle.spmv("da", rp, offs, vals, xr, alpha=1.0 / s)
+        s = np.sqrt(oracle.fold_ordered(oracle.sumsq_chunks(xr, 4096)))
+        assert s == norms[k], k
+    assert np.array_equal(x.cpu().numpy().view(np.uint64), (xr * (1.0 / s)).view(np.uint64))
+
+
+def test_c5_full_size_sampled(cuda):
+    """Config C5 on one GPU: 2^28 rows, ~2.1e9 entries, int64 rowptr."""
+    n, b, lam, kmax, seed = BANDED_CONFIGS["c5"]
+    arr = banded_arrays(n, b, lam, kmax, seed, cuda, kinds=("da",))
+    assert arr["rowptr"].dtype == torch.int64 and arr["nnz"] > 2_000_000_000
+    dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"])
+    x = normal_vector(n, 21, cuda)
+    y = torch.empty(n, dtype=torch.float64, device=cuda)
+    dm.spmv_into(x, y, 1.0, 0.0, "wstream")
+    cdf, table = poisson_cdf(lam, kmax), normal_table()
+    rng = np.random.default_rng(1)
+    rows = np.concatenate([[0, n - 1], rng.integers(0, n, 200)])
+    for r in rows.tolist():
+        offs = oracle.gen_row(n, b, kmax, seed, cdf, r)
+        cols = r + offs.astype(np.int64)
+        vals = np.array([oracle.gen_value(b, seed, r, o, table) for o in offs])
+        xs = oracle.gen_normal(21, 0, 1, table)  # warm the table path
+        xv = np.array([oracle.gen_normal(21, int(c), int(c) + 1, table)[0] for c in cols])
+        acc = 0.0
+        for v, xc in zip(vals.tolist(), xv.tolist()):
+            acc = acc + v * xc
+        assert acc == float(y[r].item()), r
+    del xs
