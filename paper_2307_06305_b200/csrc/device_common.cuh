@@ -148,27 +148,29 @@ __device__ __forceinline__ double row_sum(int order, int64_t s, int64_t e, const
   return sum_naive(s, e, get);  // NAIVE, and TREE for rows one thread owns
 }
 
-// Streaming form of the three orders for a row consumed in pieces by one
-// thread (cooperative long rows): element k (0-based within the row).
+// Streaming form of the three orders for a row consumed in order by one
+// thread (cooperative long rows): call add() once per product, in order.
 struct OrderedAcc {
-  int order;
-  int64_t len, full4;
+  int order, ph3;
+  int64_t k, full4;
   double a0, a1, a2, a3, tail;
   __device__ void init(int o, int64_t n) {
     order = o;
-    len = n;
+    ph3 = 0;
+    k = 0;
     full4 = n - (n & 3);
     a0 = a1 = a2 = a3 = tail = 0.0;
   }
-  __device__ __forceinline__ void add(int64_t k, double p) {
-    if (order == DACSR_ORDER_MACC3) {
-      const int64_t m = k % 3;
-      if (m == 0) a0 = __dadd_rn(a0, p);
-      else if (m == 1) a1 = __dadd_rn(a1, p);
+  __device__ __forceinline__ void add(double p) {
+    if (order == DACSR_ORDER_MACC3) {  // round robin a0, a1, a2 (tail lands on a0, a1)
+      if (ph3 == 0) a0 = __dadd_rn(a0, p);
+      else if (ph3 == 1) a1 = __dadd_rn(a1, p);
       else a2 = __dadd_rn(a2, p);
-    } else if (order == DACSR_ORDER_STRIP4) {
-      if (k >= full4) tail = __dadd_rn(tail, p);
-      else {
+      ph3 = ph3 == 2 ? 0 : ph3 + 1;
+    } else if (order == DACSR_ORDER_STRIP4) {  // full groups of 4, then a tail sum
+      if (k >= full4) {
+        tail = __dadd_rn(tail, p);
+      } else {
         const int m = static_cast<int>(k & 3);
         if (m == 0) a0 = __dadd_rn(a0, p);
         else if (m == 1) a1 = __dadd_rn(a1, p);
@@ -178,6 +180,7 @@ struct OrderedAcc {
     } else {
       a0 = __dadd_rn(a0, p);
     }
+    ++k;
   }
   __device__ double result() const {
     if (order == DACSR_ORDER_MACC3) return __dadd_rn(__dadd_rn(a0, a1), a2);

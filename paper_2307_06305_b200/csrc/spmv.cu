@@ -155,7 +155,7 @@ __device__ void long_row(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int64_t 
       const double* buf = scratch + (c & 1) * kLongChunk;
       const int64_t start = c * kLongChunk;
       const int n = static_cast<int>(min64(kLongChunk, len - start));
-      for (int k = 0; k < n; ++k) acc.add(start + k, buf[k]);
+      for (int k = 0; k < n; ++k) acc.add(buf[k]);
     }
     __syncthreads();
   }
@@ -344,11 +344,14 @@ struct WarpChunk {
   static constexpr int kAlign = 16 / (sizeof(VT) < sizeof(CI) ? sizeof(VT) : sizeof(CI));
 };
 
-// One row reduced by a whole warp (exact: lane 0 folds in order; TREE: shfl).
+// One row reduced by a whole warp.  TREE: lane partial sums + shfl tree.
+// Exact: 128 products per batch go to a warp scratch in shared memory and
+// lane 0 folds them in the reference order, while the next batch's gathers
+// are already in flight.
 template <int KIND, class RP, class CI, class VT>
 __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s, int64_t r,
                                            int64_t b, int64_t e, const VT* sv, const CI* si,
-                                           int64_t A, int64_t H, int lane) {
+                                           int64_t A, int64_t H, int lane, double* scratch) {
   auto get = [&](int64_t i) -> double {
     if (i < H) {
       const int k = static_cast<int>(i - A);
@@ -363,18 +366,66 @@ __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s
     if (lane == 0) epilogue(m.y, r, part, s.alpha, s.beta);
     return;
   }
+  constexpr int kPer = 4;  // products per lane per batch
   OrderedAcc acc;
   acc.init(s.order, e - b);
-  for (int64_t base = b; base < e; base += 32) {
-    const int64_t i = base + lane;
-    const double p = i < e ? get(i) : 0.0;
-    const int n = static_cast<int>(min64(32, e - base));
-    for (int k = 0; k < n; ++k) {
-      const double q = __shfl_sync(0xffffffffu, p, k);
-      if (lane == 0) acc.add(base - b + k, q);
+  double p[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int64_t i = b + u * 32 + lane;
+    p[u] = i < e ? get(i) : 0.0;
+  }
+  for (int64_t base = b; base < e; base += 32 * kPer) {
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) scratch[u * 32 + lane] = p[u];
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {  // next batch in flight during the fold
+      const int64_t i = base + 32 * kPer + u * 32 + lane;
+      p[u] = i < e ? get(i) : 0.0;
+    }
+    if (lane == 0) {
+      const int n = static_cast<int>(min64(32 * kPer, e - base));
+      for (int k = 0; k < n; ++k) acc.add(scratch[k]);
     }
   }
+  __syncwarp();
   if (lane == 0) epilogue(m.y, r, acc.result(), s.alpha, s.beta);
+}
+
+// Chunks the planner listed as not fitting the staging window: one warp per
+// chunk, rows reduced from global in the exact order, long rows by the warp.
+template <int KIND, class RP, class CI, class VT>
+__device__ __noinline__ void complex_chunks(const Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs,
+                                            int64_t re, const int64_t* __restrict__ chunks,
+                                            int64_t n_chunks, int cta, int n_ctas,
+                                            double* scratch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(n_ctas) * (blockDim.x >> 5);
+  double* wscratch = scratch + (threadIdx.x >> 5) * 128;
+  for (int64_t w = static_cast<int64_t>(cta) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       w < n_chunks; w += nw) {
+    const int64_t r = rs + 32 * ldg(chunks + w) + lane;
+    int64_t b = 0, e = 0;
+    if (r < re) {
+      b = ldg(m.rp + r);
+      e = ldg(m.rp + r + 1);
+    }
+    const bool is_long = (e - b) > s.long_len;
+    if (r < re && !is_long) {
+      auto get = [&](int64_t i) { return m.prod_global(r, i); };
+      epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
+    }
+    unsigned longs = __ballot_sync(0xffffffffu, r < re && is_long);
+    while (longs) {
+      const int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const int64_t lb = __shfl_sync(0xffffffffu, b, src), le = __shfl_sync(0xffffffffu, e, src);
+      warp_long_row(m, s, r - lane + src, lb, le, static_cast<const VT*>(nullptr),
+                    static_cast<const CI*>(nullptr), 0, 0, lane, wscratch);
+    }
+  }
 }
 
 // Fully staged row, exact order, from the warp's smem slot.
@@ -430,11 +481,20 @@ __device__ __forceinline__ bool chunk_fits(IT first, IT last, int vcap, int alig
 
 template <int KIND, class RP, class CI, class VT, int VCAP, int ORDER>
 __global__ void __launch_bounds__(256, 4)
-    wstream_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re, int64_t nnz) {
+    wstream_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re, int64_t nnz,
+                   const int64_t* complex_list, int64_t n_complex, int side_ctas) {
   using WC = WarpChunk<RP, CI, VT, VCAP>;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  // the first side_ctas CTAs take the planner's complex chunks, so they are
+  // resident from the start and overlap the streaming CTAs
+  if (static_cast<int>(blockIdx.x) < side_ctas) {
+    complex_chunks(m, s, rs, re, complex_list, n_complex, blockIdx.x, side_ctas,
+                   reinterpret_cast<double*>(dsm));
+    return;
+  }
+  const int cta = blockIdx.x - side_ctas, n_cta = gridDim.x - side_ctas;
   using IT = RP;  // entry positions fit the rowptr type
   constexpr int kRpSlot = 40;  // rowptr values per slot (33 used)
-  extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[8][WC::kSlots];
   __shared__ RP rps[8][3][kRpSlot];
   const int lane = threadIdx.x & 31;
@@ -442,8 +502,8 @@ __global__ void __launch_bounds__(256, 4)
   unsigned char* wbase = dsm + wib * WC::kWarp;
   uint64_t* bar = bars[wib];
   RP (*rp_slot)[kRpSlot] = rps[wib];
-  const int W = gridDim.x * (blockDim.x >> 5);
-  const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int W = n_cta * (blockDim.x >> 5);
+  const int gw = cta * (blockDim.x >> 5) + wib;
   const int nchunks = static_cast<int>((re - rs + 31) >> 5);
   if (gw >= nchunks) return;
   const IT last_aligned = static_cast<IT>(nnz & ~int64_t(WC::kAlign - 1));
@@ -524,39 +584,6 @@ __global__ void __launch_bounds__(256, 4)
     rslot = rnext;
   }
   cp_async_wait<0>();
-}
-
-// The chunks the planner listed as not fitting the window: one warp per
-// chunk, rows reduced from global in the exact order, long rows by the
-// whole warp.
-template <int KIND, class RP, class CI, class VT>
-__global__ void __launch_bounds__(256)
-    complex_chunks_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re,
-                          const int64_t* __restrict__ chunks, int64_t n_chunks) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-       w < n_chunks; w += nw) {
-    const int64_t r = rs + 32 * ldg(chunks + w) + lane;
-    int64_t b = 0, e = 0;
-    if (r < re) {
-      b = ldg(m.rp + r);
-      e = ldg(m.rp + r + 1);
-    }
-    const bool is_long = (e - b) > s.long_len;
-    if (r < re && !is_long) {
-      auto get = [&](int64_t i) { return m.prod_global(r, i); };
-      epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
-    }
-    unsigned longs = __ballot_sync(0xffffffffu, r < re && is_long);
-    while (longs) {
-      const int src = __ffs(longs) - 1;
-      longs &= longs - 1;
-      const int64_t lb = __shfl_sync(0xffffffffu, b, src), le = __shfl_sync(0xffffffffu, e, src);
-      warp_long_row(m, s, r - lane + src, lb, le, static_cast<const VT*>(nullptr),
-                    static_cast<const CI*>(nullptr), 0, 0, lane);
-    }
-  }
 }
 
 // planner: list the 32-row chunks that do not fit a VCAP window
@@ -756,29 +783,28 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
         return launch<KIND, RP, CI, VT>(a, r2);
       }
       const int threads = 256;
+      s.long_len = std::max<int64_t>(p->long_len, 32);
+      const int side = p->n_complex > 0
+                           ? static_cast<int>(std::min<int64_t>((p->n_complex + 7) / 8, 2 * sms))
+                           : 0;
       auto go = [&](auto kern, int per_warp) -> int {
-        const size_t smem = static_cast<size_t>(per_warp) * (threads / 32);
+        // side CTAs need 128 doubles of scratch per warp
+        const size_t smem = std::max<size_t>(static_cast<size_t>(per_warp), 128 * 8) * (threads / 32);
         const int per_sm = cached_per_sm(kern, threads, smem);
         if (per_sm < 0) return check_launch("wstream launch config");
         const int64_t chunks = (rows + 31) / 32;
-        const int64_t grid = std::min<int64_t>((chunks + 7) / 8, static_cast<int64_t>(sms) * per_sm);
-        kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), threads, smem, q.stream>>>(
-            m, s, q.rs, q.re, a->nnz);
+        // all CTAs co-resident: side CTAs take slots the streaming grid leaves
+        const int64_t slots = static_cast<int64_t>(sms) * per_sm;
+        const int64_t grid = std::min<int64_t>((chunks + 7) / 8, std::max<int64_t>(slots - side, slots / 2));
+        kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1) + side), threads, smem, q.stream>>>(
+            m, s, q.rs, q.re, a->nnz, p->complex_chunks, p->n_complex, side);
         return check_launch("wstream_kernel");
       };
-      int rc;
       if (vcap == 256)
-        rc = go(wstream_kernel<KIND, RP, CI, VT, 256, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 256>::kWarp);
-      else if (vcap == 512)
-        rc = go(wstream_kernel<KIND, RP, CI, VT, 512, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 512>::kWarp);
-      else
-        rc = go(wstream_kernel<KIND, RP, CI, VT, 1024, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 1024>::kWarp);
-      if (rc || p->n_complex == 0) return rc;
-      s.long_len = std::max<int64_t>(p->long_len, 32);
-      const int64_t grid = std::min<int64_t>((p->n_complex + 7) / 8, static_cast<int64_t>(sms) * 16);
-      complex_chunks_kernel<KIND, RP, CI, VT><<<static_cast<unsigned>(grid), threads, 0, q.stream>>>(
-          m, s, q.rs, q.re, p->complex_chunks, p->n_complex);
-      return check_launch("complex_chunks_kernel");
+        return go(wstream_kernel<KIND, RP, CI, VT, 256, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 256>::kWarp);
+      if (vcap == 512)
+        return go(wstream_kernel<KIND, RP, CI, VT, 512, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 512>::kWarp);
+      return go(wstream_kernel<KIND, RP, CI, VT, 1024, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 1024>::kWarp);
     }
     default:
       return DACSR_ERR_VARIANT;

@@ -195,3 +195,35 @@ def test_sumsq_chunks_deterministic(cuda):
     b = chunked_sumsq(y, 1 << 14)
     assert a == b
     assert abs(a - float((y * y).sum())) <= 1e-12 * a
+
+
+def test_widths_int64_rowptr_int8_offsets_int64_colids(cuda):
+    """Every device layout the library instantiates, against the oracle."""
+    from paper_2307_06305_b200.core import _trusted
+    base = laplacian_2d(100)                       # bandwidth 100: fits int8 offsets
+    x = uniform_x(base.ncols, seed=8)
+    for vdt in (np.float64, np.float32):
+        vals = base.values.astype(vdt)
+        xv = x.astype(vdt)
+        for rp_dt in (np.int32, np.int64):
+            rp = base.rowptr.astype(rp_dt)
+            mats = [
+                _trusted(dg.CsrMatrix, base.nrows, base.ncols, rp, base.colids.astype(np.int32), vals),
+                _trusted(dg.DacsrMatrix, base.nrows, base.ncols, rp,
+                         dg.to_dacsr(base, 8).colids, vals),
+                _trusted(dg.DacsrMatrix, base.nrows, base.ncols, rp,
+                         dg.to_dacsr(base, 16).colids, vals),
+                _trusted(dg.DacsrMatrix, base.nrows, base.ncols, rp,
+                         dg.to_dacsr(base, 32).colids, vals),
+            ]
+            for a in mats:
+                dm = DeviceMatrix.from_host(a, cuda)
+                if a.rowptr.dtype == np.int64:    # keep the int64 rowptr on device
+                    dm = DeviceMatrix(dm.kind, a.nrows, a.ncols,
+                                      torch.from_numpy(a.rowptr).to(cuda), dm.colids, dm.values)
+                kind = "da" if isinstance(a, dg.DacsrMatrix) else "csr"
+                ref = oracle.spmv(kind, a.rowptr, a.colids, a.values, xv)
+                for variant in ("naive", "wstream", "rowblock", "staged", "scalar"):
+                    y = dg.spmv(dm, torch.from_numpy(xv).to(cuda), variant=variant)
+                    assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (kind, variant,
+                                                                              rp_dt, vdt)

@@ -57,6 +57,14 @@ for c in args.configs.split(","):
     elif c == "c3":
         mats = banded_device("c3", dev)
         x = normal_vector(mats["da"].ncols, 17, dev)
+    elif c == "c4":
+        from paper_2307_06305_b200.workloads import skewed_rcm_laplacian
+        a, info = skewed_rcm_laplacian(2048)
+        mats = {"csr": DeviceMatrix.from_host(a), "da": DeviceMatrix.from_host(dg.to_dacsr(a, 16))}
+        x = torch.from_numpy(uniform_x(a.ncols, 1)).to(dev)
+        st = mats["da"].stats
+        print(f"# c4 stats mean {st.mean_len:.2f} max {st.max_len} cv {st.cv_len:.2f}; "
+              f"complex chunks (256) {mats['da'].chunk_plan(256).n_complex}", flush=True)
     print(f"# {c} built in {time.time()-t0:.1f}s", flush=True)
     run(c, mats, x)
     del mats
