@@ -61,11 +61,9 @@ enum {
   DACSR_VARIANT_VECTOR16 = 6,
   DACSR_VARIANT_WARP = 7,
   DACSR_VARIANT_STAGED = 8,   /* fixed rows per CTA, TMA-bulk staged (no plan)   */
-  DACSR_VARIANT_WSTREAM = 9,  /* warp streams: 32 rows/warp chunk, 128-bit loads */
-                              /* double-buffered in registers, exact orders;     */
-                              /* 256 / 512 / 1024-entry staging windows          */
-  DACSR_VARIANT_WSTREAM512 = 10,
-  DACSR_VARIANT_WSTREAM1024 = 11
+  DACSR_VARIANT_WSTREAM = 9   /* warp streams: 32-row chunks per warp, TMA bulk  */
+                              /* double-buffered per warp, exact naive order;    */
+                              /* staging window from the plan (chunk_vcap)       */
 };
 
 /* A matrix in CSR (absolute colids) or DA-CSR (colids = col - row) layout.
@@ -109,7 +107,7 @@ typedef struct {
   const int64_t* block_rows; /* device, nblocks + 1 entries (caller-owned)    */
   /* WSTREAM: 32-row chunks whose entries do not fit the staging window are
    * listed here and reduced by a side kernel (dacsr_plan_chunks).           */
-  int32_t chunk_vcap;  /* staging window (256/512/1024 entries), 0 = none     */
+  int32_t chunk_vcap;  /* staging window (entries, multiple of 16), 0 = none  */
   int32_t reserved;
   int64_t n_complex;
   const int64_t* complex_chunks; /* device, n_complex chunk indices          */
@@ -138,7 +136,8 @@ int dacsr_plan_build(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end
                      int64_t* block_rows_dev, dacsr_plan_t* out, void* stream);
 
 /* Classify the 32-row chunks of [row_start, row_end) for a WSTREAM window
- * of `vcap` entries: chunks that do not fit go to chunks_dev (capacity
+ * of `vcap` entries (multiple of 16, 64..8192): chunks that do not fit go
+ * to chunks_dev (capacity
  * ceil(rows/32) int64); count_scratch_dev is 8 device bytes.  Fills
  * inout->chunk_vcap / n_complex / complex_chunks; synchronizes `stream`. */
 int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end, int32_t vcap,

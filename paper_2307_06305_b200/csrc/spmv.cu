@@ -333,15 +333,21 @@ __global__ void __launch_bounds__(256)
 // reduced one lane per row in the exact reference order; entries past the
 // staged window come from global; rows longer than long_len are reduced by
 // the whole warp after the others.
-template <class RP, class CI, class VT, int VCAP>
+// Shared-memory layout of one warp: two slots of `vcap` entries (values,
+// then inner indices, each 16-byte aligned).  vcap is chosen per matrix by
+// the planner (a multiple of 16 covering ~99% of the 32-row chunks).
+template <class RP, class CI, class VT>
 struct WarpChunk {
-  static constexpr int kVB = VCAP * static_cast<int>(sizeof(VT));  // value bytes per slot
-  static constexpr int kIB = VCAP * static_cast<int>(sizeof(CI));  // index bytes per slot
   static constexpr int kSlots = 2;
-  static constexpr int kSlot = kVB + ((kIB + 15) & ~15);          // bytes per slot
-  static constexpr int kWarp = kSlots * kSlot;                      // bytes per warp
   // entries per 16-byte vector of the narrower array: window alignment
   static constexpr int kAlign = 16 / (sizeof(VT) < sizeof(CI) ? sizeof(VT) : sizeof(CI));
+  __host__ __device__ static constexpr int value_bytes(int vcap) {
+    return vcap * static_cast<int>(sizeof(VT));
+  }
+  __host__ __device__ static constexpr int slot_bytes(int vcap) {
+    return value_bytes(vcap) + ((vcap * static_cast<int>(sizeof(CI)) + 15) & ~15);
+  }
+  __host__ __device__ static constexpr int warp_bytes(int vcap) { return kSlots * slot_bytes(vcap); }
 };
 
 // One row reduced by a whole warp.  TREE: lane partial sums + shfl tree.
@@ -479,11 +485,12 @@ __device__ __forceinline__ bool chunk_fits(IT first, IT last, int vcap, int alig
   return last <= H;
 }
 
-template <int KIND, class RP, class CI, class VT, int VCAP, int ORDER>
+template <int KIND, class RP, class CI, class VT, int ORDER>
 __global__ void __launch_bounds__(256, 4)
     wstream_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re, int64_t nnz,
-                   const int64_t* complex_list, int64_t n_complex, int side_ctas) {
-  using WC = WarpChunk<RP, CI, VT, VCAP>;
+                   const int64_t* complex_list, int64_t n_complex, int side_ctas, int vcap) {
+  using WC = WarpChunk<RP, CI, VT>;
+  const int kSlot = WC::slot_bytes(vcap), kVB = WC::value_bytes(vcap);
   extern __shared__ __align__(128) unsigned char dsm[];
   // the first side_ctas CTAs take the planner's complex chunks, so they are
   // resident from the start and overlap the streaming CTAs
@@ -499,7 +506,7 @@ __global__ void __launch_bounds__(256, 4)
   __shared__ RP rps[8][3][kRpSlot];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  unsigned char* wbase = dsm + wib * WC::kWarp;
+  unsigned char* wbase = dsm + wib * WC::warp_bytes(vcap);
   uint64_t* bar = bars[wib];
   RP (*rp_slot)[kRpSlot] = rps[wib];
   const int W = n_cta * (blockDim.x >> 5);
@@ -530,19 +537,19 @@ __global__ void __launch_bounds__(256, 4)
   // lane 0: the chunk's entries via the TMA bulk-copy engine
   auto issue = [&](int slot, IT first) {
     const IT A = first & ~static_cast<IT>(WC::kAlign - 1);
-    IT H = A + VCAP;
+    IT H = A + vcap;
     if (H > last_aligned) H = last_aligned;
     if (H > A) {
       const uint32_t n = static_cast<uint32_t>(H - A);
-      unsigned char* dst = wbase + slot * WC::kSlot;
+      unsigned char* dst = wbase + slot * kSlot;
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&bar[slot], n * static_cast<uint32_t>(sizeof(VT) + sizeof(CI)));
       bulk_copy_g2s(dst, m.v + A, n * sizeof(VT), &bar[slot]);
-      bulk_copy_g2s(dst + WC::kVB, m.ci + A, ((n * sizeof(CI)) + 15) & ~15u, &bar[slot]);
+      bulk_copy_g2s(dst + kVB, m.ci + A, ((n * sizeof(CI)) + 15) & ~15u, &bar[slot]);
     }
   };
   auto fits = [&](int slot) {
-    return chunk_fits<IT>(rp_slot[slot][0], rp_slot[slot][32], VCAP, WC::kAlign, last_aligned);
+    return chunk_fits<IT>(rp_slot[slot][0], rp_slot[slot][32], vcap, WC::kAlign, last_aligned);
   };
 
   fetch_rp(gw, 0);
@@ -572,8 +579,8 @@ __global__ void __launch_bounds__(256, 4)
       if (r < re) {
         const IT b = rp_slot[rslot][lane], e = rp_slot[rslot][lane + 1];
         const int kk = static_cast<int>(b - A);
-        const VT* sv = reinterpret_cast<const VT*>(wbase + dslot * WC::kSlot);
-        const CI* si = reinterpret_cast<const CI*>(wbase + dslot * WC::kSlot + WC::kVB);
+        const VT* sv = reinterpret_cast<const VT*>(wbase + dslot * kSlot);
+        const CI* si = reinterpret_cast<const CI*>(wbase + dslot * kSlot + kVB);
         epilogue(m.y, r,
                  staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b),
                                    m.x + m.col(r, CI(0))),
@@ -767,13 +774,9 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       }
       return check_launch("vector_kernel");
     }
-    case DACSR_VARIANT_WSTREAM:
-    case DACSR_VARIANT_WSTREAM512:
-    case DACSR_VARIANT_WSTREAM1024: {
-      const int vcap = q.variant == DACSR_VARIANT_WSTREAM ? 256
-                       : (q.variant == DACSR_VARIANT_WSTREAM512 ? 512 : 1024);
+    case DACSR_VARIANT_WSTREAM: {
       const dacsr_plan_t* p = q.plan;
-      if (!p || p->chunk_vcap != vcap || p->row_start != q.rs || p->row_end != q.re ||
+      if (!p || p->chunk_vcap <= 0 || p->row_start != q.rs || p->row_end != q.re ||
           (p->n_complex > 0 && !p->complex_chunks) || !can_bulk)
         return DACSR_ERR_PLAN;
       if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
@@ -783,28 +786,24 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
         return launch<KIND, RP, CI, VT>(a, r2);
       }
       const int threads = 256;
+      const int vcap = p->chunk_vcap;
       s.long_len = std::max<int64_t>(p->long_len, 32);
       const int side = p->n_complex > 0
                            ? static_cast<int>(std::min<int64_t>((p->n_complex + 7) / 8, 2 * sms))
                            : 0;
-      auto go = [&](auto kern, int per_warp) -> int {
-        // side CTAs need 128 doubles of scratch per warp
-        const size_t smem = std::max<size_t>(static_cast<size_t>(per_warp), 128 * 8) * (threads / 32);
-        const int per_sm = cached_per_sm(kern, threads, smem);
-        if (per_sm < 0) return check_launch("wstream launch config");
-        const int64_t chunks = (rows + 31) / 32;
-        // all CTAs co-resident: side CTAs take slots the streaming grid leaves
-        const int64_t slots = static_cast<int64_t>(sms) * per_sm;
-        const int64_t grid = std::min<int64_t>((chunks + 7) / 8, std::max<int64_t>(slots - side, slots / 2));
-        kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1) + side), threads, smem, q.stream>>>(
-            m, s, q.rs, q.re, a->nnz, p->complex_chunks, p->n_complex, side);
-        return check_launch("wstream_kernel");
-      };
-      if (vcap == 256)
-        return go(wstream_kernel<KIND, RP, CI, VT, 256, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 256>::kWarp);
-      if (vcap == 512)
-        return go(wstream_kernel<KIND, RP, CI, VT, 512, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 512>::kWarp);
-      return go(wstream_kernel<KIND, RP, CI, VT, 1024, DACSR_ORDER_NAIVE>, WarpChunk<RP, CI, VT, 1024>::kWarp);
+      auto kern = wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE>;
+      // side CTAs need 128 doubles of scratch per warp
+      const size_t per_warp = std::max<size_t>(WarpChunk<RP, CI, VT>::warp_bytes(vcap), 128 * 8);
+      const size_t smem = per_warp * (threads / 32);
+      const int per_sm = cached_per_sm(kern, threads, smem);
+      if (per_sm < 0) return check_launch("wstream launch config");
+      const int64_t chunks = (rows + 31) / 32;
+      // all CTAs co-resident: side CTAs take slots the streaming grid leaves
+      const int64_t slots = static_cast<int64_t>(sms) * per_sm;
+      const int64_t grid = std::min<int64_t>((chunks + 7) / 8, std::max<int64_t>(slots - side, slots / 2));
+      kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1) + side), threads, smem, q.stream>>>(
+          m, s, q.rs, q.re, a->nnz, p->complex_chunks, p->n_complex, side, vcap);
+      return check_launch("wstream_kernel");
     }
     default:
       return DACSR_ERR_VARIANT;
@@ -858,11 +857,10 @@ int32_t dacsr_select_variant(const dacsr_stats_t* st, int32_t order) {
   if (!st) return DACSR_VARIANT_STAGED;
   if (order == DACSR_ORDER_TREE && st->mean_len >= 48.0)
     return st->mean_len >= 256.0 ? DACSR_VARIANT_WARP : DACSR_VARIANT_VECTOR16;
-  // warp streams: a 32-row chunk should fit its staging window ~85% of the time
+  // warp streams while a 32-row chunk's window stays small enough for
+  // several resident warps per SM (planner sizes the window per matrix)
   const double chunk = 32.0 * st->mean_len;
-  if (chunk <= 0.95 * 256) return DACSR_VARIANT_WSTREAM;
-  if (chunk <= 0.95 * 512) return DACSR_VARIANT_WSTREAM512;
-  if (chunk <= 0.95 * 1024) return DACSR_VARIANT_WSTREAM1024;
+  if (chunk <= 1536.0) return DACSR_VARIANT_WSTREAM;
   return DACSR_VARIANT_ROWBLOCK;
 }
 
@@ -870,7 +868,7 @@ int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t rs, int64_t re, int32_t v
                       int64_t* chunks_dev, void* count_scratch_dev, dacsr_plan_t* inout,
                       void* stream) {
   if (!a || !inout || !chunks_dev || !count_scratch_dev || rs < 0 || re < rs || re > a->nrows ||
-      (vcap != 256 && vcap != 512 && vcap != 1024))
+      vcap < 64 || vcap > 8192 || (vcap & 15))
     return DACSR_ERR_ARG;
   static const int kBytes[6] = {1, 2, 4, 8, 4, 8};
   if (a->values_dtype < 0 || a->values_dtype > 5 || a->colids_dtype < 0 || a->colids_dtype > 5)

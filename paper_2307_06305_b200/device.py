@@ -145,10 +145,25 @@ class DeviceMatrix:
         self.plan = plan
         return plan
 
-    _VCAP = {"wstream": 256, "wstream512": 512, "wstream1024": 1024}
+    def chunk_window(self, quantile=0.99):
+        """Staging window (entries) for WSTREAM: the given quantile of the
+        32-row chunk sizes plus the 16-byte alignment slack, rounded to 16."""
+        rs, re = self.row_start, self.row_end
+        if re <= rs:
+            return 64
+        rp = self.rowptr[rs:re + 1].to(torch.int64)
+        starts = rp[:-1:32]
+        ends = torch.cat([rp[32::32], rp[-1:]])[:starts.numel()]
+        sizes = (ends - starts).to(torch.float64)
+        q = float(torch.quantile(sizes, quantile).item()) if sizes.numel() > 1 else float(sizes.max())
+        align = 16 // min(self.values.element_size(), self.colids.element_size())
+        return int(min(8192, max(64, -(-(q + align) // 16) * 16)))
 
-    def chunk_plan(self, vcap, stream=None):
-        """Plan copy carrying the WSTREAM chunk classification for ``vcap``."""
+    def chunk_plan(self, vcap=None, stream=None):
+        """Plan copy carrying the WSTREAM chunk classification for ``vcap``
+        (default: the planner's window for this matrix)."""
+        if vcap is None:
+            vcap = self.chunk_window()
         got = self._chunk_plans.get(vcap)
         if got is not None:
             return got[0]
@@ -165,7 +180,13 @@ class DeviceMatrix:
                 ctypes.c_void_p(chunks.data_ptr()), ctypes.c_void_p(count.data_ptr()),
                 ctypes.byref(plan), _stream_ptr(stream)), "dacsr_plan_chunks")
         self._chunk_plans[vcap] = (plan, chunks)
+        self._chunk_plans[None] = self._chunk_plans[vcap]
         return plan
+
+    def set_chunk_window(self, vcap):
+        """Pin the WSTREAM staging window (entries, multiple of 16)."""
+        self.chunk_plan(int(vcap))
+        self._chunk_plans[None] = self._chunk_plans[int(vcap)]
 
     def plan_for(self, kname, row_start=None, row_end=None):
         """The plan a kernel needs (None when it needs none or the row range
@@ -174,9 +195,9 @@ class DeviceMatrix:
         re = self.row_end if row_end is None else row_end
         if self.plan is None or rs != self.plan.row_start or re != self.plan.row_end:
             return None
-        vcap = self._VCAP.get(kname)
-        if vcap is not None:
-            return self.chunk_plan(vcap)
+        if kname == "wstream":
+            got = self._chunk_plans.get(None)
+            return got[0] if got is not None else self.chunk_plan()
         return self.plan
 
     # ---- properties -----------------------------------------------------------

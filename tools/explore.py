@@ -17,7 +17,7 @@ from paper_2307_06305_b200.workloads import laplacian_2d, laplacian_3d, uniform_
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="c1,c2,c2f32,c3")
-ap.add_argument("--variants", default="naive,wstream,wstream512,wstream1024,rowblock,scalar,vector4,vector8")
+ap.add_argument("--variants", default="naive,wstream,rowblock,scalar,vector4,vector8")
 ap.add_argument("--cold", action="store_true")
 args = ap.parse_args()
 dev = torch.device("cuda")
@@ -38,6 +38,8 @@ def run(name, mats, x):
             try:
                 t = time_kernel(fn, epochs=5, warmup_iters=3, min_epoch_iters=3,
                                 min_epoch_time=0.05, cold=args.cold, graph=0 if args.cold else 20)
+            if kname == "wstream":
+                v += f"[vcap={dm.chunk_plan().chunk_vcap},cx={dm.chunk_plan().n_complex}]"
             except Exception as e:  # noqa
                 print(name, kind, v, "ERROR", e, flush=True)
                 continue
