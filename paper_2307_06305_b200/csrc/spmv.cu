@@ -785,22 +785,24 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
         r2.variant = p->block_rows ? DACSR_VARIANT_ROWBLOCK : DACSR_VARIANT_STAGED;
         return launch<KIND, RP, CI, VT>(a, r2);
       }
-      const int threads = 256;
       const int vcap = p->chunk_vcap;
-      s.long_len = std::max<int64_t>(p->long_len, 32);
-      const int side = p->n_complex > 0
-                           ? static_cast<int>(std::min<int64_t>((p->n_complex + 7) / 8, 2 * sms))
-                           : 0;
-      auto kern = wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE>;
       // side CTAs need 128 doubles of scratch per warp
       const size_t per_warp = std::max<size_t>(WarpChunk<RP, CI, VT>::warp_bytes(vcap), 128 * 8);
-      const size_t smem = per_warp * (threads / 32);
+      // up to 8 warps per CTA within ~200 KiB of shared memory
+      const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp)));
+      const int threads = 32 * warps;
+      s.long_len = std::max<int64_t>(p->long_len, 32);
+      const int side = p->n_complex > 0
+                           ? static_cast<int>(std::min<int64_t>((p->n_complex + warps - 1) / warps, 2 * sms))
+                           : 0;
+      auto kern = wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE>;
+      const size_t smem = per_warp * warps;
       const int per_sm = cached_per_sm(kern, threads, smem);
       if (per_sm < 0) return check_launch("wstream launch config");
       const int64_t chunks = (rows + 31) / 32;
       // all CTAs co-resident: side CTAs take slots the streaming grid leaves
       const int64_t slots = static_cast<int64_t>(sms) * per_sm;
-      const int64_t grid = std::min<int64_t>((chunks + 7) / 8, std::max<int64_t>(slots - side, slots / 2));
+      const int64_t grid = std::min<int64_t>((chunks + warps - 1) / warps, std::max<int64_t>(slots - side, slots / 2));
       kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1) + side), threads, smem, q.stream>>>(
           m, s, q.rs, q.re, a->nnz, p->complex_chunks, p->n_complex, side, vcap);
       return check_launch("wstream_kernel");

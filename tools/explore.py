@@ -38,11 +38,11 @@ def run(name, mats, x):
             try:
                 t = time_kernel(fn, epochs=5, warmup_iters=3, min_epoch_iters=3,
                                 min_epoch_time=0.05, cold=args.cold, graph=0 if args.cold else 20)
-            if kname == "wstream":
-                v += f"[vcap={dm.chunk_plan().chunk_vcap},cx={dm.chunk_plan().n_complex}]"
             except Exception as e:  # noqa
                 print(name, kind, v, "ERROR", e, flush=True)
                 continue
+            if kname == "wstream":
+                v += f"[vcap={dm.chunk_plan().chunk_vcap},cx={dm.chunk_plan().n_complex}]"
             rec = dict(config=name, kind=kind, variant=v, us=t * 1e6, gbs=tr / t / 1e9,
                        bytes=tr, cold=args.cold, plan_cap=dm.plan.cap if dm.plan else None)
             out.append(rec)
