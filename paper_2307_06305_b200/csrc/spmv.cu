@@ -792,16 +792,18 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp)));
       const int threads = 32 * warps;
       s.long_len = std::max<int64_t>(p->long_len, 32);
-      const int side = p->n_complex > 0
-                           ? static_cast<int>(std::min<int64_t>((p->n_complex + warps - 1) / warps, 2 * sms))
-                           : 0;
       auto kern = wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE>;
       const size_t smem = per_warp * warps;
       const int per_sm = cached_per_sm(kern, threads, smem);
       if (per_sm < 0) return check_launch("wstream launch config");
       const int64_t chunks = (rows + 31) / 32;
-      // all CTAs co-resident: side CTAs take slots the streaming grid leaves
+      // all CTAs co-resident; the complex chunks get at most 1/8 of the
+      // slots (they loop), the streaming grid the rest
       const int64_t slots = static_cast<int64_t>(sms) * per_sm;
+      const int side = p->n_complex > 0
+                           ? static_cast<int>(std::min<int64_t>((p->n_complex + warps - 1) / warps,
+                                                                std::max<int64_t>(1, slots / 8)))
+                           : 0;
       const int64_t grid = std::min<int64_t>((chunks + warps - 1) / warps, std::max<int64_t>(slots - side, slots / 2));
       kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1) + side), threads, smem, q.stream>>>(
           m, s, q.rs, q.re, a->nnz, p->complex_chunks, p->n_complex, side, vcap);
