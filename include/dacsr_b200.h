@@ -108,7 +108,7 @@ typedef struct {
   /* WSTREAM: 32-row chunks whose entries do not fit the staging window are
    * listed here and reduced by a side kernel (dacsr_plan_chunks).           */
   int32_t chunk_vcap;  /* staging window (entries, multiple of 16), 0 = none  */
-  int32_t reserved;
+  int32_t chunk_rows;  /* rows per warp chunk: 32 (1 per lane) or 64 (2)     */
   int64_t n_complex;
   const int64_t* complex_chunks; /* device, n_complex chunk indices          */
 } dacsr_plan_t;
@@ -135,14 +135,14 @@ int dacsr_plan_build(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end
                      int64_t entry_start, int64_t entry_end, int32_t cap, int32_t long_len,
                      int64_t* block_rows_dev, dacsr_plan_t* out, void* stream);
 
-/* Classify the 32-row chunks of [row_start, row_end) for a WSTREAM window
- * of `vcap` entries (multiple of 16, 64..8192): chunks that do not fit go
- * to chunks_dev (capacity
- * ceil(rows/32) int64); count_scratch_dev is 8 device bytes.  Fills
+/* Classify the chunk_rows-row chunks (32 or 64) of [row_start, row_end)
+ * for a WSTREAM window of `vcap` entries (multiple of 16, 64..16384): chunks
+ * that do not fit go to chunks_dev (capacity ceil(rows/chunk_rows) int64);
+ * count_scratch_dev is 8 device bytes.  Fills
  * inout->chunk_vcap / n_complex / complex_chunks; synchronizes `stream`. */
-int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end, int32_t vcap,
-                      int64_t* chunks_dev, void* count_scratch_dev, dacsr_plan_t* inout,
-                      void* stream);
+int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end,
+                      int32_t chunk_rows, int32_t vcap, int64_t* chunks_dev,
+                      void* count_scratch_dev, dacsr_plan_t* inout, void* stream);
 
 /* Variant the library would run for DACSR_VARIANT_AUTO. */
 int32_t dacsr_select_variant(const dacsr_stats_t* stats, int32_t order);

@@ -60,7 +60,7 @@ class Plan(ctypes.Structure):
                 ("entry_base", ctypes.c_int64), ("entry_end", ctypes.c_int64),
                 ("nblocks", ctypes.c_int64), ("cap", ctypes.c_int32),
                 ("long_len", ctypes.c_int32), ("block_rows", ctypes.c_void_p),
-                ("chunk_vcap", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("chunk_vcap", ctypes.c_int32), ("chunk_rows", ctypes.c_int32),
                 ("n_complex", ctypes.c_int64), ("complex_chunks", ctypes.c_void_p)]
 
 
@@ -83,7 +83,8 @@ _SIGNATURES = {
     "dacsr_plan_build": ([_P(Matrix), _i64, _i64, _i64, _i64, _i32, _i32, _vp, _P(Plan), _vp],
                          ctypes.c_int),
     "dacsr_select_variant": ([_P(Stats), _i32], _i32),
-    "dacsr_plan_chunks": ([_P(Matrix), _i64, _i64, _i32, _vp, _vp, _P(Plan), _vp], ctypes.c_int),
+    "dacsr_plan_chunks": ([_P(Matrix), _i64, _i64, _i32, _i32, _vp, _vp, _P(Plan), _vp],
+                          ctypes.c_int),
     "dacsr_spmv": ([_P(Matrix), _P(Plan), _i32, _i32, _vp, _i64, _vp, _d, _d, _i64, _i64, _vp],
                    ctypes.c_int),
     "dacsr_scale": ([_vp, _i32, _i64, _d, _vp], ctypes.c_int),

@@ -405,14 +405,15 @@ __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s
 template <int KIND, class RP, class CI, class VT>
 __device__ __noinline__ void complex_chunks(const Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs,
                                             int64_t re, const int64_t* __restrict__ chunks,
-                                            int64_t n_chunks, int cta, int n_ctas,
-                                            double* scratch) {
+                                            int64_t n_chunks, int rows_per_chunk, int cta,
+                                            int n_ctas, double* scratch) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = static_cast<int64_t>(n_ctas) * (blockDim.x >> 5);
   double* wscratch = scratch + (threadIdx.x >> 5) * 128;
+  const int sub = rows_per_chunk / 32;  // 32-row pieces per listed chunk
   for (int64_t w = static_cast<int64_t>(cta) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       w < n_chunks; w += nw) {
-    const int64_t r = rs + 32 * ldg(chunks + w) + lane;
+       w < n_chunks * sub; w += nw) {
+    const int64_t r = rs + rows_per_chunk * ldg(chunks + w / sub) + 32 * (w % sub) + lane;
     int64_t b = 0, e = 0;
     if (r < re) {
       b = ldg(m.rp + r);
@@ -485,23 +486,24 @@ __device__ __forceinline__ bool chunk_fits(IT first, IT last, int vcap, int alig
   return last <= H;
 }
 
-template <int KIND, class RP, class CI, class VT, int ORDER>
+template <int KIND, class RP, class CI, class VT, int ORDER, int RPL>
 __global__ void __launch_bounds__(256, 4)
     wstream_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re, int64_t nnz,
                    const int64_t* complex_list, int64_t n_complex, int side_ctas, int vcap) {
   using WC = WarpChunk<RP, CI, VT>;
+  constexpr int kRows = 32 * RPL;         // rows per chunk (RPL per lane)
+  constexpr int kRpSlot = kRows + 8;      // rowptr values per slot (kRows + 1 used)
   const int kSlot = WC::slot_bytes(vcap), kVB = WC::value_bytes(vcap);
   extern __shared__ __align__(128) unsigned char dsm[];
   // the first side_ctas CTAs take the planner's complex chunks, so they are
   // resident from the start and overlap the streaming CTAs
   if (static_cast<int>(blockIdx.x) < side_ctas) {
-    complex_chunks(m, s, rs, re, complex_list, n_complex, blockIdx.x, side_ctas,
+    complex_chunks(m, s, rs, re, complex_list, n_complex, kRows, blockIdx.x, side_ctas,
                    reinterpret_cast<double*>(dsm));
     return;
   }
   const int cta = blockIdx.x - side_ctas, n_cta = gridDim.x - side_ctas;
   using IT = RP;  // entry positions fit the rowptr type
-  constexpr int kRpSlot = 40;  // rowptr values per slot (33 used)
   __shared__ __align__(8) uint64_t bars[8][WC::kSlots];
   __shared__ RP rps[8][3][kRpSlot];
   const int lane = threadIdx.x & 31;
@@ -511,7 +513,7 @@ __global__ void __launch_bounds__(256, 4)
   RP (*rp_slot)[kRpSlot] = rps[wib];
   const int W = n_cta * (blockDim.x >> 5);
   const int gw = cta * (blockDim.x >> 5) + wib;
-  const int nchunks = static_cast<int>((re - rs + 31) >> 5);
+  const int nchunks = static_cast<int>((re - rs + kRows - 1) / kRows);
   if (gw >= nchunks) return;
   const IT last_aligned = static_cast<IT>(nnz & ~int64_t(WC::kAlign - 1));
 
@@ -519,14 +521,17 @@ __global__ void __launch_bounds__(256, 4)
     for (int k = 0; k < WC::kSlots; ++k) mbar_init(&bar[k], 1);
     mbar_fence_init();
   }
-  // rowptr slice of chunk c: lane l copies rowptr[rs+32c+l+1] (clamped),
-  // lane 0 also rowptr[rs+32c]
+  // rowptr slice of chunk c: lane l copies rowptr[rs + kRows*c + 32q + l + 1]
+  // (clamped) for q < RPL, lane 0 also rowptr[rs + kRows*c]
   auto fetch_rp = [&](int c, int slot) {
     if (c < nchunks) {
-      const int64_t row0 = rs + 32 * static_cast<int64_t>(c);
-      const RP* src = m.rp + min64(row0 + lane + 1, re);
-      if constexpr (sizeof(RP) == 8) cp_async_8(&rp_slot[slot][lane + 1], src);
-      else cp_async_4(&rp_slot[slot][lane + 1], src);
+      const int64_t row0 = rs + kRows * static_cast<int64_t>(c);
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const RP* src = m.rp + min64(row0 + 32 * q + lane + 1, re);
+        if constexpr (sizeof(RP) == 8) cp_async_8(&rp_slot[slot][32 * q + lane + 1], src);
+        else cp_async_4(&rp_slot[slot][32 * q + lane + 1], src);
+      }
       if (lane == 0) {
         if constexpr (sizeof(RP) == 8) cp_async_8(&rp_slot[slot][0], m.rp + row0);
         else cp_async_4(&rp_slot[slot][0], m.rp + row0);
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(256, 4)
     }
   };
   auto fits = [&](int slot) {
-    return chunk_fits<IT>(rp_slot[slot][0], rp_slot[slot][32], vcap, WC::kAlign, last_aligned);
+    return chunk_fits<IT>(rp_slot[slot][0], rp_slot[slot][kRows], vcap, WC::kAlign, last_aligned);
   };
 
   fetch_rp(gw, 0);
@@ -568,23 +573,26 @@ __global__ void __launch_bounds__(256, 4)
     __syncwarp();
     if (lane == 0 && c + W < nchunks && fits(rnext)) issue(dslot ^ 1, rp_slot[rnext][0]);
     fetch_rp(c + 2 * W, rnn);
-    if (fits(rslot)) {  // warp-uniform: complex chunks belong to the side kernel
+    if (fits(rslot)) {  // warp-uniform: complex chunks belong to the side CTAs
       const IT first = rp_slot[rslot][0];
       const IT A = first & ~static_cast<IT>(WC::kAlign - 1);
-      if (rp_slot[rslot][32] > A) {  // non-empty chunk
+      if (rp_slot[rslot][kRows] > A) {  // non-empty chunk
         mbar_wait(&bar[dslot], (phase >> dslot) & 1u);
         phase ^= 1u << dslot;
       }
-      const int64_t r = rs + 32 * static_cast<int64_t>(c) + lane;
-      if (r < re) {
-        const IT b = rp_slot[rslot][lane], e = rp_slot[rslot][lane + 1];
-        const int kk = static_cast<int>(b - A);
-        const VT* sv = reinterpret_cast<const VT*>(wbase + dslot * kSlot);
-        const CI* si = reinterpret_cast<const CI*>(wbase + dslot * kSlot + kVB);
-        epilogue(m.y, r,
-                 staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b),
-                                   m.x + m.col(r, CI(0))),
-                 s.alpha, s.beta);
+      const VT* sv = reinterpret_cast<const VT*>(wbase + dslot * kSlot);
+      const CI* si = reinterpret_cast<const CI*>(wbase + dslot * kSlot + kVB);
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int64_t r = rs + kRows * static_cast<int64_t>(c) + 32 * q + lane;
+        if (r < re) {
+          const IT b = rp_slot[rslot][32 * q + lane], e = rp_slot[rslot][32 * q + lane + 1];
+          const int kk = static_cast<int>(b - A);
+          epilogue(m.y, r,
+                   staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b),
+                                     m.x + m.col(r, CI(0))),
+                   s.alpha, s.beta);
+        }
       }
     }
     __syncwarp();
@@ -596,14 +604,14 @@ __global__ void __launch_bounds__(256, 4)
 // planner: list the 32-row chunks that do not fit a VCAP window
 template <class RP>
 __global__ void classify_chunks_kernel(const RP* __restrict__ rp, int64_t rs, int64_t re,
-                                       int vcap, int align, int64_t last_aligned,
+                                       int rows, int vcap, int align, int64_t last_aligned,
                                        int64_t* out, unsigned long long* count) {
-  const int64_t nchunks = (re - rs + 31) >> 5;
+  const int64_t nchunks = (re - rs + rows - 1) / rows;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < nchunks;
        c += stride) {
-    const int64_t first = static_cast<int64_t>(rp[rs + 32 * c]);
-    const int64_t last = static_cast<int64_t>(rp[min64(rs + 32 * c + 32, re)]);
+    const int64_t first = static_cast<int64_t>(rp[rs + rows * c]);
+    const int64_t last = static_cast<int64_t>(rp[min64(rs + rows * c + rows, re)]);
     if (!chunk_fits<int64_t>(first, last, vcap, align, last_aligned)) {
       const unsigned long long slot = atomicAdd(count, 1ull);
       out[slot] = c;
@@ -776,7 +784,8 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
     }
     case DACSR_VARIANT_WSTREAM: {
       const dacsr_plan_t* p = q.plan;
-      if (!p || p->chunk_vcap <= 0 || p->row_start != q.rs || p->row_end != q.re ||
+      if (!p || p->chunk_vcap <= 0 || (p->chunk_rows != 32 && p->chunk_rows != 64) ||
+          p->row_start != q.rs || p->row_end != q.re ||
           (p->n_complex > 0 && !p->complex_chunks) || !can_bulk)
         return DACSR_ERR_PLAN;
       if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
@@ -792,11 +801,12 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp)));
       const int threads = 32 * warps;
       s.long_len = std::max<int64_t>(p->long_len, 32);
-      auto kern = wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE>;
+      auto kern = p->chunk_rows == 64 ? wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE, 2>
+                                      : wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE, 1>;
       const size_t smem = per_warp * warps;
       const int per_sm = cached_per_sm(kern, threads, smem);
       if (per_sm < 0) return check_launch("wstream launch config");
-      const int64_t chunks = (rows + 31) / 32;
+      const int64_t chunks = (rows + p->chunk_rows - 1) / p->chunk_rows;
       // all CTAs co-resident; the complex chunks get at most 1/8 of the
       // slots (they loop), the streaming grid the rest
       const int64_t slots = static_cast<int64_t>(sms) * per_sm;
@@ -868,11 +878,11 @@ int32_t dacsr_select_variant(const dacsr_stats_t* st, int32_t order) {
   return DACSR_VARIANT_ROWBLOCK;
 }
 
-int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t rs, int64_t re, int32_t vcap,
-                      int64_t* chunks_dev, void* count_scratch_dev, dacsr_plan_t* inout,
-                      void* stream) {
+int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t rs, int64_t re, int32_t chunk_rows,
+                      int32_t vcap, int64_t* chunks_dev, void* count_scratch_dev,
+                      dacsr_plan_t* inout, void* stream) {
   if (!a || !inout || !chunks_dev || !count_scratch_dev || rs < 0 || re < rs || re > a->nrows ||
-      vcap < 64 || vcap > 8192 || (vcap & 15))
+      vcap < 64 || vcap > 16384 || (vcap & 15) || (chunk_rows != 32 && chunk_rows != 64))
     return DACSR_ERR_ARG;
   static const int kBytes[6] = {1, 2, 4, 8, 4, 8};
   if (a->values_dtype < 0 || a->values_dtype > 5 || a->colids_dtype < 0 || a->colids_dtype > 5)
@@ -887,15 +897,17 @@ int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t rs, int64_t re, int32_t v
     set_last_error("plan_chunks memset", e);
     return DACSR_ERR_CUDA;
   }
-  const int64_t nchunks = (re - rs + 31) / 32;
+  const int64_t nchunks = (re - rs + chunk_rows - 1) / chunk_rows;
   if (nchunks > 0) {
     const int g = static_cast<int>(std::min<int64_t>((nchunks + 255) / 256, 148 * 32));
     if (a->rowptr_dtype == DACSR_I64)
       classify_chunks_kernel<int64_t><<<g, 256, 0, st>>>(static_cast<const int64_t*>(a->rowptr), rs, re,
-                                                         vcap, align, last_aligned, chunks_dev, count);
+                                                         chunk_rows, vcap, align, last_aligned,
+                                                         chunks_dev, count);
     else if (a->rowptr_dtype == DACSR_I32)
       classify_chunks_kernel<int32_t><<<g, 256, 0, st>>>(static_cast<const int32_t*>(a->rowptr), rs, re,
-                                                         vcap, align, last_aligned, chunks_dev, count);
+                                                         chunk_rows, vcap, align, last_aligned,
+                                                         chunks_dev, count);
     else
       return DACSR_ERR_DTYPE;
     int rc = check_launch("classify_chunks_kernel");
@@ -909,6 +921,7 @@ int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t rs, int64_t re, int32_t v
     return DACSR_ERR_CUDA;
   }
   inout->chunk_vcap = vcap;
+  inout->chunk_rows = chunk_rows;
   inout->n_complex = static_cast<int64_t>(h);
   inout->complex_chunks = chunks_dev;
   return DACSR_OK;

@@ -145,48 +145,59 @@ class DeviceMatrix:
         self.plan = plan
         return plan
 
-    def chunk_window(self, quantile=0.99):
+    def chunk_rows(self):
+        """Rows per warp chunk: 64 (two per lane) for short rows, else 32."""
+        st = self.stats or self.analyze()
+        return 64 if 32.0 * st.mean_len <= 320.0 else 32
+
+    def chunk_window(self, rows=None, quantile=0.99):
         """Staging window (entries) for WSTREAM: the given quantile of the
-        32-row chunk sizes plus the 16-byte alignment slack, rounded to 16."""
+        chunk entry counts plus the 16-byte alignment slack, rounded to 16."""
+        rows = rows or self.chunk_rows()
         rs, re = self.row_start, self.row_end
         if re <= rs:
             return 64
         rp = self.rowptr[rs:re + 1].to(torch.int64)
-        starts = rp[:-1:32]
-        ends = torch.cat([rp[32::32], rp[-1:]])[:starts.numel()]
+        starts = rp[:-1:rows]
+        ends = torch.cat([rp[rows::rows], rp[-1:]])[:starts.numel()]
         sizes = (ends - starts).to(torch.float64)
         q = float(torch.quantile(sizes, quantile).item()) if sizes.numel() > 1 else float(sizes.max())
         align = 16 // min(self.values.element_size(), self.colids.element_size())
-        return int(min(8192, max(64, -(-(q + align) // 16) * 16)))
+        return int(min(16384, max(64, -(-(q + align) // 16) * 16)))
 
-    def chunk_plan(self, vcap=None, stream=None):
-        """Plan copy carrying the WSTREAM chunk classification for ``vcap``
-        (default: the planner's window for this matrix)."""
+    def chunk_plan(self, vcap=None, rows=None, stream=None):
+        """Plan copy carrying the WSTREAM chunk classification for a window
+        of ``vcap`` entries over ``rows``-row chunks (defaults: planner's)."""
+        rows = rows or self.chunk_rows()
         if vcap is None:
-            vcap = self.chunk_window()
-        got = self._chunk_plans.get(vcap)
+            vcap = self.chunk_window(rows)
+        key = (vcap, rows)
+        got = self._chunk_plans.get(key)
         if got is not None:
             return got[0]
         if self.plan is None:
             self.build_plan(stream=stream)
         plan = _native.Plan()
         ctypes.memmove(ctypes.byref(plan), ctypes.byref(self.plan), ctypes.sizeof(plan))
-        nchunks = max(1, (self.row_end - self.row_start + 31) // 32)
+        nchunks = max(1, (self.row_end - self.row_start + rows - 1) // rows)
         chunks = torch.empty(nchunks, dtype=torch.int64, device=self.device)
         count = torch.empty(1, dtype=torch.int64, device=self.device)
         with torch.cuda.device(self.device):
             _native.check(_native.lib().dacsr_plan_chunks(
-                ctypes.byref(self.desc), self.row_start, self.row_end, int(vcap),
+                ctypes.byref(self.desc), self.row_start, self.row_end, int(rows), int(vcap),
                 ctypes.c_void_p(chunks.data_ptr()), ctypes.c_void_p(count.data_ptr()),
                 ctypes.byref(plan), _stream_ptr(stream)), "dacsr_plan_chunks")
-        self._chunk_plans[vcap] = (plan, chunks)
-        self._chunk_plans[None] = self._chunk_plans[vcap]
+        self._chunk_plans[key] = (plan, chunks)
+        if None not in self._chunk_plans:
+            self._chunk_plans[None] = self._chunk_plans[key]
         return plan
 
-    def set_chunk_window(self, vcap):
-        """Pin the WSTREAM staging window (entries, multiple of 16)."""
-        self.chunk_plan(int(vcap))
-        self._chunk_plans[None] = self._chunk_plans[int(vcap)]
+    def set_chunk_window(self, vcap, rows=None):
+        """Pin the WSTREAM staging window (entries, multiple of 16) and the
+        rows per warp chunk (32 or 64)."""
+        rows = rows or self.chunk_rows()
+        self.chunk_plan(int(vcap), rows)
+        self._chunk_plans[None] = self._chunk_plans[(int(vcap), rows)]
 
     def plan_for(self, kname, row_start=None, row_end=None):
         """The plan a kernel needs (None when it needs none or the row range

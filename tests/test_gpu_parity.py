@@ -176,10 +176,11 @@ def test_skewed_long_rows_bit_exact(cuda):  # noqa: C901
     # and large (none do)
     dm = DeviceMatrix.from_host(d, cuda)
     xd = torch.from_numpy(x).to(cuda)
-    for vcap in (64, 96, 160, 1024, 4096):
-        dm.set_chunk_window(vcap)
-        y = dg.spmv(dm, xd, variant="wstream")
-        assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), vcap
+    for rows in (32, 64):
+        for vcap in (64, 96, 160, 1024, 4096):
+            dm.set_chunk_window(vcap, rows)
+            y = dg.spmv(dm, xd, variant="wstream")
+            assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (vcap, rows)
     for variant in ("rowblock_tree", "vector8", "warp"):
         y = dg.spmv(dg.to_dacsr(a, 16), x, variant=variant)
         ref = oracle.spmv("da", a.rowptr, dg.to_dacsr(a, 16).colids, a.values, x)
