@@ -556,12 +556,18 @@ __global__ void __launch_bounds__(256, 4)
   auto fits = [&](int slot) {
     return chunk_fits<IT>(rp_slot[slot][0], rp_slot[slot][kRows], vcap, WC::kAlign, last_aligned);
   };
+  // a chunk's entries are copied (and waited for) iff it fits and is not
+  // empty; both sides evaluate this same predicate
+  auto staged = [&](int slot) {
+    const IT A = rp_slot[slot][0] & ~static_cast<IT>(WC::kAlign - 1);
+    return fits(slot) && rp_slot[slot][kRows] > A;
+  };
 
   fetch_rp(gw, 0);
   fetch_rp(gw + W, 1);
   cp_async_wait<1>();
   __syncwarp();
-  if (lane == 0 && fits(0)) issue(0, rp_slot[0][0]);
+  if (lane == 0 && staged(0)) issue(0, rp_slot[0][0]);
   uint32_t phase = 0;
   int rslot = 0;
   int k = 0;
@@ -571,12 +577,12 @@ __global__ void __launch_bounds__(256, 4)
     const int rnn = rnext == 2 ? 0 : rnext + 1;
     cp_async_wait<0>();  // rowptr of chunk c + W (issued last iteration)
     __syncwarp();
-    if (lane == 0 && c + W < nchunks && fits(rnext)) issue(dslot ^ 1, rp_slot[rnext][0]);
+    if (lane == 0 && c + W < nchunks && staged(rnext)) issue(dslot ^ 1, rp_slot[rnext][0]);
     fetch_rp(c + 2 * W, rnn);
     if (fits(rslot)) {  // warp-uniform: complex chunks belong to the side CTAs
       const IT first = rp_slot[rslot][0];
       const IT A = first & ~static_cast<IT>(WC::kAlign - 1);
-      if (rp_slot[rslot][kRows] > A) {  // non-empty chunk
+      if (staged(rslot)) {
         mbar_wait(&bar[dslot], (phase >> dslot) & 1u);
         phase ^= 1u << dslot;
       }

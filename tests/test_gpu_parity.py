@@ -236,3 +236,27 @@ def test_widths_int64_rowptr_int8_offsets_int64_colids(cuda):
                     y = dg.spmv(dm, torch.from_numpy(xv).to(cuda), variant=variant)
                     assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (kind, variant,
                                                                               rp_dt, vdt)
+
+
+def test_wstream_empty_rows_and_chunks(cuda):
+    """Empty rows, whole empty 32/64-row chunks, and an empty tail."""
+    rng = np.random.default_rng(12)
+    n = 5000
+    counts = rng.integers(0, 6, n)
+    counts[100:300] = 0          # empty chunks
+    counts[-200:] = 0            # empty tail
+    rp = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    cols = np.concatenate([np.sort(rng.choice(np.arange(max(0, r - 40), min(n, r + 41)),
+                                              size=k, replace=False))
+                           for r, k in enumerate(counts)]).astype(np.int32)
+    a = dg.CsrMatrix(n, n, rp, cols, rng.standard_normal(len(cols)))
+    d = dg.to_dacsr(a, 16)
+    x = uniform_x(n, 3)
+    ref = oracle.spmv("da", d.rowptr, d.colids, d.values, x)
+    dm = DeviceMatrix.from_host(d, cuda)
+    xd = torch.from_numpy(x).to(cuda)
+    for rows in (32, 64):
+        for vcap in (64, 128, 512):
+            dm.set_chunk_window(vcap, rows)
+            y = dg.spmv(dm, xd, variant="wstream")
+            assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (rows, vcap)
