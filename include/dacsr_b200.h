@@ -219,6 +219,14 @@ int dacsr_counts_to_rowptr(const int32_t* counts, int64_t m, void* rowptr,
                            int32_t rowptr_dtype, void* temp, size_t* temp_bytes,
                            void* stream);
 
+/* ---- measurement ---------------------------------------------------------- */
+/* Read-stream probe: warps stream `bytes` of `buf` into shared memory with
+ * TMA bulk copies of `chunk` bytes (two slots per warp, 8 warps per CTA,
+ * `ctas` CTAs) — the WSTREAM data path without compute.  `sink` is a device
+ * double that is never written in practice. */
+int dacsr_stream_probe(const void* buf, int64_t bytes, int32_t chunk, int32_t ctas, double* sink,
+                       void* stream);
+
 /* ---- host-side reordering (reference reorder.py:70-220), CPU only -------- */
 /* Symmetrized adjacency of a square CSR pattern (pattern of A + A^T, no
  * self-loops, ascending, deduplicated).  Two calls: first with

@@ -98,6 +98,7 @@ _SIGNATURES = {
     "dacsr_gen_normal": ([_u64, _i64, _i64, _vp, _vp, _i32, _vp], ctypes.c_int),
     "dacsr_counts_to_rowptr": ([_vp, _i64, _vp, _i32, _vp, _P(ctypes.c_size_t), _vp],
                                ctypes.c_int),
+    "dacsr_stream_probe": ([_vp, _i64, _i32, _i32, _vp, _vp], ctypes.c_int),
     "dacsr_host_adjacency": ([_i64, _vp, _vp, _vp, _vp], ctypes.c_int),
     "dacsr_host_rcm": ([_i64, _vp, _vp, _vp], ctypes.c_int),
     "dacsr_host_permute": ([_i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp], ctypes.c_int),

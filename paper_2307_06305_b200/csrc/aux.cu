@@ -332,3 +332,61 @@ int dacsr_csr_to_da(const dacsr_matrix_t* a, void* offsets, int32_t odt, void* s
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Read-bandwidth probe (measurement only): every warp streams `chunk`-byte
+// pieces of a buffer into shared memory with TMA bulk copies, two slots per
+// warp, exactly like the WSTREAM data path but with no compute.  Gives the
+// read-stream ceiling the SpMV kernels are measured against.
+namespace dacsr {
+namespace {
+__global__ void __launch_bounds__(256) stream_probe_kernel(const unsigned char* buf, int64_t bytes,
+                                                           int chunk, double* sink) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[8][2];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* wb = dsm + wib * 2 * chunk;
+  const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib;
+  const int64_t n = bytes / chunk;
+  if (lane == 0) {
+    mbar_init(&bars[wib][0], 1);
+    mbar_init(&bars[wib][1], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  auto issue = [&](int slot, int64_t c) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[wib][slot], chunk);
+    bulk_copy_g2s(wb + slot * chunk, buf + c * chunk, chunk, &bars[wib][slot]);
+  };
+  if (lane == 0 && gw < n) issue(0, gw);
+  uint32_t phase = 0;
+  double acc = 0.0;
+  int k = 0;
+  for (int64_t c = gw; c < n; c += W, ++k) {
+    const int slot = k & 1;
+    if (lane == 0 && c + W < n) issue(slot ^ 1, c + W);
+    mbar_wait(&bars[wib][slot], (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+    acc += reinterpret_cast<const double*>(wb + slot * chunk)[lane];
+    __syncwarp();
+  }
+  if (acc == 12345.678) *sink = acc;  // keep the loads observable
+}
+}  // namespace
+}  // namespace dacsr
+
+extern "C" int dacsr_stream_probe(const void* buf, int64_t bytes, int32_t chunk, int32_t ctas,
+                                  double* sink, void* stream) {
+  using namespace dacsr;
+  if (!buf || bytes <= 0 || chunk < 256 || (chunk & 15) || chunk > 12288 || ctas <= 0)
+    return DACSR_ERR_ARG;
+  const size_t smem = static_cast<size_t>(chunk) * 2 * 8;
+  if (cudaFuncSetAttribute(stream_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return check_launch("stream_probe attribute");
+  stream_probe_kernel<<<ctas, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const unsigned char*>(buf), bytes, chunk, sink);
+  return check_launch("stream_probe_kernel");
+}
