@@ -111,6 +111,8 @@ typedef struct {
   int32_t chunk_rows;  /* rows per warp chunk: 32 (1 per lane) or 64 (2)     */
   int64_t n_complex;
   const int64_t* complex_chunks; /* device, n_complex chunk indices          */
+  int32_t ctas_per_sm; /* WSTREAM resident CTAs per SM (0 = occupancy max)    */
+  int32_t reserved;
 } dacsr_plan_t;
 
 const char* dacsr_version(void);

@@ -61,7 +61,8 @@ class Plan(ctypes.Structure):
                 ("nblocks", ctypes.c_int64), ("cap", ctypes.c_int32),
                 ("long_len", ctypes.c_int32), ("block_rows", ctypes.c_void_p),
                 ("chunk_vcap", ctypes.c_int32), ("chunk_rows", ctypes.c_int32),
-                ("n_complex", ctypes.c_int64), ("complex_chunks", ctypes.c_void_p)]
+                ("n_complex", ctypes.c_int64), ("complex_chunks", ctypes.c_void_p),
+                ("ctas_per_sm", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 def typed_kernel_names():

@@ -810,8 +810,9 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       auto kern = p->chunk_rows == 64 ? wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE, 2>
                                       : wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE, 1>;
       const size_t smem = per_warp * warps;
-      const int per_sm = cached_per_sm(kern, threads, smem);
+      int per_sm = cached_per_sm(kern, threads, smem);
       if (per_sm < 0) return check_launch("wstream launch config");
+      if (p->ctas_per_sm > 0) per_sm = std::min(per_sm, static_cast<int>(p->ctas_per_sm));
       const int64_t chunks = (rows + p->chunk_rows - 1) / p->chunk_rows;
       // all CTAs co-resident; the complex chunks get at most 1/8 of the
       // slots (they loop), the streaming grid the rest

@@ -188,10 +188,17 @@ class DeviceMatrix:
                 ctypes.byref(self.desc), self.row_start, self.row_end, int(rows), int(vcap),
                 ctypes.c_void_p(chunks.data_ptr()), ctypes.c_void_p(count.data_ptr()),
                 ctypes.byref(plan), _stream_ptr(stream)), "dacsr_plan_chunks")
+        plan.ctas_per_sm = getattr(self, "_ctas_per_sm", 0)
         self._chunk_plans[key] = (plan, chunks)
         if None not in self._chunk_plans:
             self._chunk_plans[None] = self._chunk_plans[key]
         return plan
+
+    def set_ctas_per_sm(self, n):
+        """Cap WSTREAM's resident CTAs per SM (0 = occupancy maximum)."""
+        for plan, _ in self._chunk_plans.values():
+            plan.ctas_per_sm = int(n)
+        self._ctas_per_sm = int(n)
 
     def set_chunk_window(self, vcap, rows=None):
         """Pin the WSTREAM staging window (entries, multiple of 16) and the
