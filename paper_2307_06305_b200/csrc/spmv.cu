@@ -569,41 +569,50 @@ __global__ void __launch_bounds__(256, 4)
   fetch_rp(gw + W, 1);
   cp_async_wait<1>();
   __syncwarp();
-  if (lane == 0 && staged(0)) issue(0, rp_slot[0][0]);
+  // per chunk, `fits` and `staged` are evaluated once (when its rowptr
+  // slice lands) and carried to the iteration that consumes the chunk
+  bool fits_cur = fits(0), staged_cur = staged(0);
+  if (lane == 0 && staged_cur) issue(0, rp_slot[0][0]);
   uint32_t phase = 0;
   int rslot = 0;
   int k = 0;
+  const VT* __restrict__ xbase = m.x + m.xoff;
   for (int c = gw; c < nchunks; c += W, ++k) {
     const int dslot = k & 1;
     const int rnext = rslot == 2 ? 0 : rslot + 1;
     const int rnn = rnext == 2 ? 0 : rnext + 1;
     cp_async_wait<0>();  // rowptr of chunk c + W (issued last iteration)
     __syncwarp();
-    if (lane == 0 && c + W < nchunks && staged(rnext)) issue(dslot ^ 1, rp_slot[rnext][0]);
+    const bool has_next = c + W < nchunks;
+    const bool fits_next = has_next && fits(rnext);
+    const bool staged_next = fits_next && staged(rnext);
+    if (lane == 0 && staged_next) issue(dslot ^ 1, rp_slot[rnext][0]);
     fetch_rp(c + 2 * W, rnn);
-    if (fits(rslot)) {  // warp-uniform: complex chunks belong to the side CTAs
-      const IT first = rp_slot[rslot][0];
-      const IT A = first & ~static_cast<IT>(WC::kAlign - 1);
-      if (staged(rslot)) {
+    if (fits_cur) {  // warp-uniform: complex chunks belong to the side CTAs
+      if (staged_cur) {
         mbar_wait(&bar[dslot], (phase >> dslot) & 1u);
         phase ^= 1u << dslot;
       }
+      const IT A = rp_slot[rslot][0] & ~static_cast<IT>(WC::kAlign - 1);
       const VT* sv = reinterpret_cast<const VT*>(wbase + dslot * kSlot);
       const CI* si = reinterpret_cast<const CI*>(wbase + dslot * kSlot + kVB);
+      const int64_t row0 = rs + kRows * static_cast<int64_t>(c);
 #pragma unroll
       for (int q = 0; q < RPL; ++q) {
-        const int64_t r = rs + kRows * static_cast<int64_t>(c) + 32 * q + lane;
-        if (r < re) {
-          const IT b = rp_slot[rslot][32 * q + lane], e = rp_slot[rslot][32 * q + lane + 1];
+        const int rl = 32 * q + lane;
+        if (row0 + rl < re) {
+          const int64_t r = row0 + rl;
+          const IT b = rp_slot[rslot][rl], e = rp_slot[rslot][rl + 1];
           const int kk = static_cast<int>(b - A);
-          epilogue(m.y, r,
-                   staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b),
-                                     m.x + m.col(r, CI(0))),
+          const VT* xr = KIND == DACSR_KIND_DA ? xbase + r : xbase;
+          epilogue(m.y, r, staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b), xr),
                    s.alpha, s.beta);
         }
       }
     }
     __syncwarp();
+    fits_cur = fits_next;
+    staged_cur = staged_next;
     rslot = rnext;
   }
   cp_async_wait<0>();
