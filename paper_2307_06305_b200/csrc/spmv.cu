@@ -438,19 +438,72 @@ __device__ __noinline__ void complex_chunks(const Mat<KIND, RP, CI, VT> m, Scal 
 // Fully staged row, exact order, from the warp's smem slot.
 // xr = &x[column base of this row]; all gathers of a batch are issued before
 // the first product is folded.
+// Eight gathers x[xr + off[u]] for u < cnt, issued by ONE asm statement so
+// the compiler cannot interleave the fold between them: all eight are in
+// flight before the first product is formed (ILP 8 per lane).
+__device__ __forceinline__ void gather8(const double* xr, const int* off, int cnt, double* v) {
+  const double* p[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) p[u] = xr + off[u];
+  asm volatile(
+      "{\n\t.reg .pred q<8>;\n\t"
+      "setp.gt.s32 q0, %16, 0;\n\tsetp.gt.s32 q1, %16, 1;\n\t"
+      "setp.gt.s32 q2, %16, 2;\n\tsetp.gt.s32 q3, %16, 3;\n\t"
+      "setp.gt.s32 q4, %16, 4;\n\tsetp.gt.s32 q5, %16, 5;\n\t"
+      "setp.gt.s32 q6, %16, 6;\n\tsetp.gt.s32 q7, %16, 7;\n\t"
+      "@q0 ld.global.nc.f64 %0, [%8];\n\t@q1 ld.global.nc.f64 %1, [%9];\n\t"
+      "@q2 ld.global.nc.f64 %2, [%10];\n\t@q3 ld.global.nc.f64 %3, [%11];\n\t"
+      "@q4 ld.global.nc.f64 %4, [%12];\n\t@q5 ld.global.nc.f64 %5, [%13];\n\t"
+      "@q6 ld.global.nc.f64 %6, [%14];\n\t@q7 ld.global.nc.f64 %7, [%15];\n\t}"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]),
+        "=d"(v[7])
+      : "l"(p[0]), "l"(p[1]), "l"(p[2]), "l"(p[3]), "l"(p[4]), "l"(p[5]), "l"(p[6]), "l"(p[7]),
+        "r"(cnt));
+}
+__device__ __forceinline__ void gather8(const float* xr, const int* off, int cnt, float* v) {
+  const float* p[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) p[u] = xr + off[u];
+  asm volatile(
+      "{\n\t.reg .pred q<8>;\n\t"
+      "setp.gt.s32 q0, %16, 0;\n\tsetp.gt.s32 q1, %16, 1;\n\t"
+      "setp.gt.s32 q2, %16, 2;\n\tsetp.gt.s32 q3, %16, 3;\n\t"
+      "setp.gt.s32 q4, %16, 4;\n\tsetp.gt.s32 q5, %16, 5;\n\t"
+      "setp.gt.s32 q6, %16, 6;\n\tsetp.gt.s32 q7, %16, 7;\n\t"
+      "@q0 ld.global.nc.f32 %0, [%8];\n\t@q1 ld.global.nc.f32 %1, [%9];\n\t"
+      "@q2 ld.global.nc.f32 %2, [%10];\n\t@q3 ld.global.nc.f32 %3, [%11];\n\t"
+      "@q4 ld.global.nc.f32 %4, [%12];\n\t@q5 ld.global.nc.f32 %5, [%13];\n\t"
+      "@q6 ld.global.nc.f32 %6, [%14];\n\t@q7 ld.global.nc.f32 %7, [%15];\n\t}"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7])
+      : "l"(p[0]), "l"(p[1]), "l"(p[2]), "l"(p[3]), "l"(p[4]), "l"(p[5]), "l"(p[6]), "l"(p[7]),
+        "r"(cnt));
+}
+
 template <int ORDER, class CI, class VT>
 __device__ __forceinline__ double staged_dot(const VT* pv, const CI* pi, int n,
                                              const VT* __restrict__ xr) {
   if constexpr (ORDER == DACSR_ORDER_NAIVE) {
     double acc = 0.0;
     for (int j = 0; j < n; j += 8) {
+      const int cnt = n - j;
       VT xv[8];
+      if constexpr (sizeof(VT) == 8) {
+        // f64: one asm statement for the 8 gathers (measured: 7 of 8 issued
+        // before the first fold vs 4+4 from the plain loop; C2 33.2 -> 32.4 us)
+        int off[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) off[u] = u < cnt ? static_cast<int>(pi[j + u]) : 0;
+        gather8(xr, off, cnt, xv);
+      } else {
+        // f32: the plain loop measured faster (26.9 vs 29.1 us on C2 f32)
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u < cnt) xv[u] = ldg(xr + pi[j + u]);
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (j + u < n) xv[u] = ldg(xr + pi[j + u]);
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j + u < n) acc = __dadd_rn(acc, product(pv[j + u], xv[u]));
+        if (u < cnt) acc = __dadd_rn(acc, product(pv[j + u], xv[u]));
     }
     return acc;
   } else {
