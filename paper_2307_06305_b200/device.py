@@ -76,6 +76,7 @@ class DeviceMatrix:
         self.plan = None
         self._block_rows = None
         self._chunk_plans = {}
+        self.tuned_kernel = None
         if plan:
             self.build_plan(cap=cap, long_len=long_len)
 
@@ -193,6 +194,25 @@ class DeviceMatrix:
         if None not in self._chunk_plans:
             self._chunk_plans[None] = self._chunk_plans[key]
         return plan
+
+    def autotune(self, candidates=("wstream", "scalar", "rowblock", "staged"), cold=False,
+                 x=None, reps=5):
+        """Time the exact naive-order kernels on this matrix and remember the
+        fastest for variant "naive"/"auto" (all give bit-identical results,
+        so this only changes speed).  Returns {kernel: seconds}."""
+        from .harness import time_kernel
+        if x is None:
+            x = torch.ones(self.ncols, dtype=self.values.dtype, device=self.device)
+        y = torch.empty(self.nrows, dtype=self.values.dtype, device=self.device)
+        times = {}
+        for k in candidates:
+            if k in ("wstream", "rowblock") and self.plan is None:
+                continue
+            fn = lambda k=k: self.spmv_into(x, y, 1.0, 0.0, k, 0)
+            times[k] = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
+                                   min_epoch_time=0.0, cold=cold, graph=0 if cold else reps)
+        self.tuned_kernel = min(times, key=times.get)
+        return times
 
     def set_ctas_per_sm(self, n):
         """Cap WSTREAM's resident CTAs per SM (0 = occupancy maximum)."""

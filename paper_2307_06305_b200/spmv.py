@@ -122,6 +122,8 @@ def resolve_variant(variant):
 def kernel_for(dm, kname, order):
     """Concrete kernel name for a resolved (name, order) on this matrix."""
     if kname == "exact":
+        if order == _native.ORDER_NAIVE and getattr(dm, "tuned_kernel", None):
+            return dm.tuned_kernel      # DeviceMatrix.autotune() picked it
         if dm.stats is None:
             return "staged"
         kname = _CODE_NAME[_native.lib().dacsr_select_variant(dm.stats, order)]
