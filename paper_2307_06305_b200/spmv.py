@@ -36,6 +36,7 @@ from .device import DeviceMatrix, _stream_ptr
 from .errors import DimensionMismatch, UnsupportedScalarWidth
 
 ENV_FLAG = "DACSR_BACKEND"
+STREAMED_MIN_ROWS = 1 << 18  # host-array calls at least this tall use the streamed path
 
 SERIAL_VARIANTS = ("naive", "shifted_base", "multi_accumulator_3", "strip_mined_4")
 
@@ -215,6 +216,15 @@ def spmv(a, x, y=None, alpha=1.0, beta=0.0, variant="naive", backend=None, *, st
             _native.check(_native.lib().dacsr_scale(
                 _native.ctypes.c_void_p(y_dev.data_ptr()), _native.dtype_code(dm.values.dtype),
                 nrows, beta, _stream_ptr(stream)), "dacsr_scale")
+        elif (not isinstance(x, torch.Tensor) and not isinstance(y, torch.Tensor)
+              and nrows >= STREAMED_MIN_ROWS and dm.nnz and stream is None):
+            # host in, host out: x streams in by row pieces while earlier
+            # pieces compute and their y streams back (hostpath.py)
+            from .hostpath import streamed
+            y_host = y if y.flags.c_contiguous and y.flags.writeable else None
+            if y_host is None:
+                raise ValueError("y must be a writable C-contiguous array")
+            return streamed(dm).run(np.ascontiguousarray(x), y_host, alpha, beta, kname, order)
         else:
             x_dev = x.contiguous() if isinstance(x, torch.Tensor) else _to_device(x, dev)
             if y_dev is None:

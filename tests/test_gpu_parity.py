@@ -260,3 +260,27 @@ def test_wstream_empty_rows_and_chunks(cuda):
             dm.set_chunk_window(vcap, rows)
             y = dg.spmv(dm, xd, variant="wstream")
             assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (rows, vcap)
+
+
+def test_streamed_host_path_bit_exact(cuda):
+    """spmv(A, x_host, y_host) above STREAMED_MIN_ROWS pipelines the copies
+    by row pieces; results equal the device path bit for bit (pinned and
+    pageable host buffers, beta = 0 and beta != 0, DA and CSR)."""
+    from paper_2307_06305_b200.spmv import STREAMED_MIN_ROWS
+    csr = laplacian_2d(640)                       # 409,600 rows >= 2^18
+    assert csr.nrows >= STREAMED_MIN_ROWS
+    x = uniform_x(csr.ncols, 5)
+    y0 = np.random.default_rng(6).uniform(-1, 1, csr.nrows)
+    for a in (dg.to_dacsr(csr, 16), csr):
+        kind = "da" if isinstance(a, dg.DacsrMatrix) else "csr"
+        for alpha, beta in ((1.0, 0.0), (0.5, -2.0)):
+            ref = oracle.spmv(kind, a.rowptr, a.colids, a.values, x, y0.copy(), alpha, beta)
+            y = y0.copy()
+            dg.spmv(a, x, y, alpha, beta)
+            assert np.array_equal(bits(y), bits(ref)), (kind, beta)
+            xp = torch.empty(len(x), dtype=torch.float64, pin_memory=True)
+            yp = torch.empty(len(y0), dtype=torch.float64, pin_memory=True)
+            xp.numpy()[:] = x
+            yp.numpy()[:] = y0
+            out = dg.spmv(a, xp.numpy(), yp.numpy(), alpha, beta)
+            assert np.array_equal(bits(out), bits(ref)), (kind, beta, "pinned")
