@@ -23,7 +23,7 @@ from .spmv import kernel_for
 class StreamedHost:
     """Per-DeviceMatrix resources of the streamed host path (cached)."""
 
-    def __init__(self, dm, pieces=8):
+    def __init__(self, dm, pieces=4):  # measured on C2: 1 -> 0.72 ms, 4 -> 0.61 ms, 16 -> 0.93 ms
         from .device import DeviceMatrix, bandwidth_device
         self.dm = dm
         n = dm.nrows
