@@ -8,6 +8,17 @@
 
 #include "dacsr_b200.h"
 
+// Bounds-checked build (compute-sanitizer is unavailable on this pool):
+// -DDACSR_CHECKED turns every DACSR_CHECK into a trap on violation.
+#ifdef DACSR_CHECKED
+#define DACSR_CHECK(cond) \
+  do {                    \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define DACSR_CHECK(cond) ((void)0)
+#endif
+
 namespace dacsr {
 
 // ---------------------------------------------------------------- errors

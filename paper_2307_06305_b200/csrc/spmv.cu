@@ -68,12 +68,22 @@ struct Mat {
   const VT* __restrict__ x;
   VT* __restrict__ y;
   int64_t xoff;
+  int64_t nrows, ncols, nnz;  // bounds for the checked build
   __device__ __forceinline__ int64_t col(int64_t r, CI c) const {
     return (KIND == DACSR_KIND_DA ? r + static_cast<int64_t>(c) : static_cast<int64_t>(c)) +
            xoff;
   }
+  // entry i of row r: checked build verifies i, the row and the column
+  __device__ __forceinline__ void check(int64_t r, int64_t i, CI c) const {
+    DACSR_CHECK(r >= 0 && r < nrows);
+    DACSR_CHECK(i >= 0 && i < nnz);
+    DACSR_CHECK(col(r, c) - xoff >= 0 && col(r, c) - xoff < ncols);
+    (void)r; (void)i; (void)c;
+  }
   __device__ __forceinline__ double prod_global(int64_t r, int64_t i) const {
-    return product(ldg(v + i), ldg(x + col(r, ldg(ci + i))));
+    const CI c = ldg(ci + i);
+    check(r, i, c);
+    return product(ldg(v + i), ldg(x + col(r, c)));
   }
 };
 
@@ -114,6 +124,8 @@ struct StagedGet {
   __device__ __forceinline__ double operator()(int64_t i) const {
     if (i < hi) {
       const int k = static_cast<int>(i - lo);
+      DACSR_CHECK(i >= lo);
+      m.check(r, i, si[k]);
       return product(sv[k], ldg(m.x + m.col(r, si[k])));
     }
     return m.prod_global(r, i);
@@ -361,6 +373,8 @@ __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s
   auto get = [&](int64_t i) -> double {
     if (i < H) {
       const int k = static_cast<int>(i - A);
+      DACSR_CHECK(i >= A);
+      m.check(r, i, si[k]);
       return product(sv[k], ldg(m.x + m.col(r, si[k])));
     }
     return m.prod_global(r, i);
@@ -657,6 +671,11 @@ __global__ void __launch_bounds__(256, 4)
           const int64_t r = row0 + rl;
           const IT b = rp_slot[rslot][rl], e = rp_slot[rslot][rl + 1];
           const int kk = static_cast<int>(b - A);
+          DACSR_CHECK(kk >= 0 && kk + (e - b) <= vcap && e >= b);
+#ifdef DACSR_CHECKED
+          for (int j = 0; j < static_cast<int>(e - b); ++j)
+            m.check(r, b + j, reinterpret_cast<const CI*>(wbase + dslot * kSlot + kVB)[kk + j]);
+#endif
           const VT* xr = KIND == DACSR_KIND_DA ? xbase + r : xbase;
           epilogue(m.y, r, staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b), xr),
                    s.alpha, s.beta);
@@ -781,7 +800,9 @@ template <int KIND, class RP, class CI, class VT>
 int launch(const dacsr_matrix_t* a, const Req& q) {
   Mat<KIND, RP, CI, VT> m{static_cast<const RP*>(a->rowptr), static_cast<const CI*>(a->colids),
                           static_cast<const VT*>(a->values), static_cast<const VT*>(q.x),
-                          static_cast<VT*>(q.y), q.xoff};
+                          static_cast<VT*>(q.y), q.xoff, a->nrows,
+                          a->ncols > 0 ? a->ncols : INT64_MAX,
+                          a->nnz > 0 ? a->nnz : INT64_MAX};
   const int64_t rows = q.re - q.rs;
   if (rows <= 0) return DACSR_OK;
   const int order = q.order;
