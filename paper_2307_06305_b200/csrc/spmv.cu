@@ -564,9 +564,14 @@ __global__ void __launch_bounds__(256, 4)
   constexpr int kRpSlot = kRows + 8;      // rowptr values per slot (kRows + 1 used)
   const int kSlot = WC::slot_bytes(vcap), kVB = WC::value_bytes(vcap);
   extern __shared__ __align__(128) unsigned char dsm[];
+  // Programmatic dependent launch: the next launch in the stream may start
+  // its prologue (matrix-only reads) while this grid drains; x and y are
+  // touched only after griddepcontrol.wait (the previous grid complete).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // the first side_ctas CTAs take the planner's complex chunks, so they are
   // resident from the start and overlap the streaming CTAs
   if (static_cast<int>(blockIdx.x) < side_ctas) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     complex_chunks(m, s, rs, re, complex_list, n_complex, kRows, blockIdx.x, side_ctas,
                    reinterpret_cast<double*>(dsm));
     return;
@@ -640,6 +645,7 @@ __global__ void __launch_bounds__(256, 4)
   // slice lands) and carried to the iteration that consumes the chunk
   bool fits_cur = fits(0), staged_cur = staged(0);
   if (lane == 0 && staged_cur) issue(0, rp_slot[0][0]);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y from here on
   uint32_t phase = 0;
   int rslot = 0;
   int k = 0;
@@ -907,8 +913,24 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
                                                                 std::max<int64_t>(1, slots / 8)))
                            : 0;
       const int64_t grid = std::min<int64_t>((chunks + warps - 1) / warps, std::max<int64_t>(slots - side, slots / 2));
-      kern<<<static_cast<unsigned>(std::max<int64_t>(grid, 1) + side), threads, smem, q.stream>>>(
-          m, s, q.rs, q.re, a->nnz, p->complex_chunks, p->n_complex, side, vcap);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(grid, 1) + side));
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = q.stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      const int64_t nnz = a->nnz;
+      const int64_t* cl = p->complex_chunks;
+      const int64_t ncx = p->n_complex;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, q.rs, q.re, nnz, cl, ncx, side, vcap);
+      if (e != cudaSuccess) {
+        set_last_error("wstream_kernel launch", e);
+        return DACSR_ERR_CUDA;
+      }
       return check_launch("wstream_kernel");
     }
     default:
