@@ -36,6 +36,7 @@ import numpy as np  # noqa: E402
 
 SPMV_PER_STEP = 100
 FALLBACK_HBM = 6650.0
+READ_CEILING_GBS = 7268.4  # tools/peaks.py on this pool's B200 (profiles/ncu_summary.json)
 
 
 def parse():
@@ -416,6 +417,10 @@ def run_ours(args):
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(kname + ":c2:da"),
                      "peak_source": peak_src, "bytes_per_launch": t_da,
                      "frac_of_nominal_8TBs": round(achieved / 8000.0, 4),
+                     "frac_of_tma_read_ceiling": round(achieved / READ_CEILING_GBS, 4),
+                     "read_ceiling_note": f"{READ_CEILING_GBS} GB/s = pure TMA bulk-copy "
+                                          "read stream measured by tools/peaks.py (SpMV is "
+                                          "~91% reads; the copy peak counts writes too)",
                      "cold_single_spmv_gbs": round(t_da / cold_da / 1e9, 1)},
         "csr_comparator": {"kernel": kc, "value": round(SPMV_PER_STEP * t_csr / step_c / 1e9, 1),
                            "unit": "GB/s", "bytes_per_spmv": t_csr,
