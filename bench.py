@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-suite", action="store_true", help="skip the C1/C2-f32/C3/C4 lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--suite", default="c1,c2f32,c3,c4")
+    ap.add_argument("--distributed", action="store_true",
+                    help="use the row-block/halo path even at one rank (plumbing check)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
                     help="c2: 100 back-to-back SpMVs (default); c5: 50-iteration power "
                          "iteration on the 2^28-row banded matrix")
@@ -367,7 +369,7 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.workload == "c5" and world == 1:
         return run_c5(args, world, rank, local)
-    if world > 1:
+    if world > 1 or args.distributed:
         from paper_2307_06305_b200 import distributed
         return distributed.bench_main(args, rank, world, local)
     torch.cuda.set_device(local)
