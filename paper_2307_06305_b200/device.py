@@ -76,6 +76,8 @@ class DeviceMatrix:
         self.plan = None
         self._block_rows = None
         self._chunk_plans = {}
+        self._launch_cache = {}
+        self._spmv_fn = _native.lib().dacsr_spmv
         self.tuned_kernel = None
         if plan:
             self.build_plan(cap=cap, long_len=long_len)
@@ -144,6 +146,8 @@ class DeviceMatrix:
                 ctypes.c_void_p(self._block_rows.data_ptr()), ctypes.byref(plan),
                 _stream_ptr(stream)), "dacsr_plan_build")
         self.plan = plan
+        if hasattr(self, "_launch_cache"):
+            self._launch_cache.clear()
         return plan
 
     def chunk_rows(self):
@@ -191,6 +195,7 @@ class DeviceMatrix:
                 ctypes.byref(plan), _stream_ptr(stream)), "dacsr_plan_chunks")
         plan.ctas_per_sm = getattr(self, "_ctas_per_sm", 0)
         self._chunk_plans[key] = (plan, chunks)
+        self._launch_cache.clear()
         if None not in self._chunk_plans:
             self._chunk_plans[None] = self._chunk_plans[key]
         return plan
@@ -219,6 +224,7 @@ class DeviceMatrix:
         for plan, _ in self._chunk_plans.values():
             plan.ctas_per_sm = int(n)
         self._ctas_per_sm = int(n)
+        self._launch_cache.clear()
 
     def set_chunk_window(self, vcap, rows=None):
         """Pin the WSTREAM staging window (entries, multiple of 16) and the
@@ -226,6 +232,7 @@ class DeviceMatrix:
         rows = rows or self.chunk_rows()
         self.chunk_plan(int(vcap), rows)
         self._chunk_plans[None] = self._chunk_plans[(int(vcap), rows)]
+        self._launch_cache.clear()
 
     def plan_for(self, kname, row_start=None, row_end=None):
         """The plan a kernel needs (None when it needs none or the row range
@@ -263,16 +270,31 @@ class DeviceMatrix:
     def spmv_into(self, x, y, alpha=1.0, beta=0.0, variant="rowblock", order=0, x_offset=0,
                   row_start=None, row_end=None, stream=None):
         """Launch y = alpha*A@x + beta*y on device tensors (no validation
-        beyond the C ABI's; ``spmv`` is the validating entry point)."""
-        code = _native.VARIANT_CODES[variant] if isinstance(variant, str) else int(variant)
-        rs = self.row_start if row_start is None else int(row_start)
-        re = self.row_end if row_end is None else int(row_end)
-        plan = self.plan_for(variant if isinstance(variant, str) else "", rs, re)
-        _native.check(_native.lib().dacsr_spmv(
-            ctypes.byref(self.desc), ctypes.byref(plan) if plan is not None else None, code,
-            int(order), ctypes.c_void_p(x.data_ptr()) if x is not None else None, int(x_offset),
-            ctypes.c_void_p(y.data_ptr()), float(alpha), float(beta), rs, re,
-            _stream_ptr(stream)), "dacsr_spmv")
+        beyond the C ABI's; ``spmv`` is the validating entry point).
+
+        The (variant, order, row range) -> (code, plan) resolution is cached
+        per matrix, so a launch costs one ctypes call (a few microseconds of
+        host time — it sits between back-to-back kernels)."""
+        key = (variant, order, row_start, row_end)
+        rec = self._launch_cache.get(key)
+        if rec is None:
+            code = _native.VARIANT_CODES[variant] if isinstance(variant, str) else int(variant)
+            rs = self.row_start if row_start is None else int(row_start)
+            re = self.row_end if row_end is None else int(row_end)
+            plan = self.plan_for(variant if isinstance(variant, str) else "", rs, re)
+            rec = (ctypes.byref(self.desc), ctypes.byref(plan) if plan is not None else None,
+                   code, int(order), rs, re, plan)
+            self._launch_cache[key] = rec
+        desc, plan_ref, code, order_code, rs, re, _ = rec
+        if stream is None:
+            sp = torch.cuda.current_stream(self.device).cuda_stream
+        else:
+            sp = stream.cuda_stream
+        status = self._spmv_fn(desc, plan_ref, code, order_code,
+                               x.data_ptr() if x is not None else None, x_offset,
+                               y.data_ptr(), alpha, beta, rs, re, sp)
+        if status:
+            _native.check(status, "dacsr_spmv")
         return y
 
     def __repr__(self):
