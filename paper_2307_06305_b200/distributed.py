@@ -188,14 +188,25 @@ class CudaLocalOp:
 
 
 def dist_spmv(op, x_ext, y, alpha, plan, group=None, overlap=True):
-    """y = alpha * A_local x (x_ext's own rows current, halo exchanged here)."""
+    """y = alpha * A_local x (x_ext's own rows current, halo exchanged here).
+
+    CUDA: the interior rows run on the current stream while the halo is in
+    flight on NCCL's stream; the two boundary strips run on a side stream
+    that waits only for the exchange, so they overlap the interior's tail."""
     if overlap and x_ext.is_cuda:
+        cur = torch.cuda.current_stream(x_ext.device)
+        side = getattr(op, "side_stream", None)
+        if side is None:
+            side = op.side_stream = torch.cuda.Stream(x_ext.device)
+        side.wait_stream(cur)                      # x_ext / y ready for the strips
         reqs = exchange_halo(x_ext, plan, group)   # NCCL stream
         op.spmv_part(0, x_ext, y, alpha)           # interior: no halo needed
-        for r in reqs:
-            r.wait()                               # compute stream waits on NCCL
-        op.spmv_part(1, x_ext, y, alpha)
-        op.spmv_part(2, x_ext, y, alpha)
+        with torch.cuda.stream(side):
+            for r in reqs:
+                r.wait()                           # side stream waits on NCCL
+            op.spmv_part(1, x_ext, y, alpha, stream=side)
+            op.spmv_part(2, x_ext, y, alpha, stream=side)
+        cur.wait_stream(side)
     else:
         for r in exchange_halo(x_ext, plan, group):
             r.wait()
