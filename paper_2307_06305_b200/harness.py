@@ -110,7 +110,7 @@ class ClockSampler:
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0, period_ms=100):
+    def __init__(self, index=0, period_ms=20):
         self.index = index
         self.period_ms = period_ms
         self.rows = []
@@ -147,8 +147,9 @@ class ClockSampler:
     def summary(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
-                    "samples": 0}
+            why = "nvidia-smi unavailable" if self._proc is None else \
+                "no sample: timed region shorter than the sampling period"
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [why], "samples": 0}
         sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
         mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
         reasons = sorted({names[i] for r in self.rows for i in range(4)
