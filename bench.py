@@ -10,8 +10,8 @@ Workload (BASELINE.json configs[1], C2): 3D 7-point Laplacian on a 128^3
 grid, n = 2,097,152, nnz = 14,581,760, float64, DA-CSR with int16 offsets
 (bandwidth 16384), x ~ U[-1,1] (seed 1).  One step = 100 back-to-back
 SpMVs y = A·x (one CUDA graph of 100 launches).  The DA matrix is 188 MB
-(> the 126 MB L2) and L2 is additionally flushed (2x L2 write) before every
-step, outside the step's CUDA events.
+(> the 126 MB L2) and L2 is additionally flushed (a read of 2x L2, which
+leaves clean lines) before every step, outside the step's CUDA events.
 
 value    = whole-job algorithmic GB/s = steps * 100 * spmv_traffic bytes / sum of
            step times (model.py / reference model.py:103-110: (n+1)*4 + nnz*(2+8)
@@ -413,7 +413,7 @@ def run_ours(args):
         "config": {"workload": "C2: 3D 7-pt Laplacian 128^3 (n=2097152, nnz=14581760), DA-CSR "
                                "i16 offsets, f64, x~U[-1,1] seed 1",
                    "spmv_per_step": SPMV_PER_STEP, "kernel": kname,
-                   "l2": "188 MB matrix > 126 MB L2; L2 flushed (2x L2 write) before every step",
+                   "l2": "188 MB matrix > 126 MB L2; L2 flushed (read of 2x L2, clean lines) before every step",
                    "parallelism": "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(kname + ":c2:da"),

@@ -24,14 +24,19 @@ def l2_bytes(device=None):
 
 
 def flush_l2(device=None, stream=None):
-    """Overwrite 2x L2 worth of memory (evicts every matrix/vector line)."""
+    """Evict L2 by READING 2x L2 worth of memory.
+
+    A write-based flush leaves L2 full of dirty lines whose write-back then
+    lands inside the next timed region; reading leaves clean lines, so the
+    measured kernel pays only for its own traffic."""
     device = torch.device(device or "cuda")
     buf = _flush_buf.get(device)
     if buf is None:
-        buf = torch.empty(2 * l2_bytes(device) // 4, dtype=torch.int32, device=device)
-        _flush_buf[device] = buf
+        buf = torch.ones(2 * l2_bytes(device) // 4, dtype=torch.int32, device=device)
+        _flush_buf[device] = (buf, torch.empty(1, dtype=torch.int64, device=device))
+    buf, out = _flush_buf[device]
     with torch.cuda.stream(stream or torch.cuda.current_stream(device)):
-        buf.fill_(1)
+        torch.sum(buf, out=out)
 
 
 class GraphBatch:
