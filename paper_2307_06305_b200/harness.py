@@ -33,10 +33,10 @@ def flush_l2(device=None, stream=None):
     buf = _flush_buf.get(device)
     if buf is None:
         buf = torch.ones(2 * l2_bytes(device) // 4, dtype=torch.int32, device=device)
-        _flush_buf[device] = (buf, torch.empty(1, dtype=torch.int64, device=device))
+        _flush_buf[device] = (buf, torch.empty((), dtype=torch.int64, device=device))
     buf, out = _flush_buf[device]
     with torch.cuda.stream(stream or torch.cuda.current_stream(device)):
-        torch.sum(buf, out=out)
+        torch.sum(buf, 0, out=out)
 
 
 class GraphBatch:
