@@ -270,6 +270,18 @@ def slab_laplacian_3d(nx, nz_total, z0, z1, dtype=np.float64):
     return rowptr.astype(np.int32), colids, sub.values[e0:e1]
 
 
+def _peak_gbs():
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0
+
+
 def bench_main(args, rank, world, local):
     """Weak scaling: rank p owns planes [128p, 128p+128) of a 128x128x(128N)
     Laplacian (C2 per rank), DA-CSR f64; a step = 100 distributed SpMVs
@@ -322,8 +334,9 @@ def bench_main(args, rank, world, local):
         torch.cuda.synchronize()
         run, graphed = g.replay, True
     except Exception as exc:  # NCCL P2P capture unsupported: stay eager
+        import sys
         print(f"[rank {rank}] graph capture failed ({type(exc).__name__}: {exc}); eager",
-              flush=True)
+              file=sys.stderr, flush=True)
     dist.barrier()
     times = []
     with ClockSampler(local) as clocks:
@@ -341,6 +354,26 @@ def bench_main(args, rank, world, local):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total = float(t.item())
     value = world * args.steps * 100 * traffic / total / 1e9
+
+    # e2e: host buffers through the same path — every SpMV copies this rank's
+    # x rows in (pinned) and its y rows out; 10 SpMVs per step, max over ranks
+    e2e_spmv = 10
+    xh = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
+    yh = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
+    xh.copy_(x.cpu())
+    e2e_steps = max(2, args.steps // 5)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for _ in range(e2e_spmv):
+            bufs[0][own].copy_(xh, non_blocking=True)
+            dist_spmv(op, bufs[0], bufs[1][own], 1.0, plan)
+            yh.copy_(bufs[1][own], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    e2e_gbs = world * e2e_steps * e2e_spmv * traffic / float(el.item()) / 1e9
     if rank == 0:
         line = {
             "metric": "SpMV effective HBM GB/s (DA-CSR i16, f64)", "value": round(value, 1),
@@ -352,6 +385,15 @@ def bench_main(args, rank, world, local):
                                    "send/recv) overlapped with interior rows",
                        "spmv_per_step": 100, "parallelism": f"row blocks x{world}",
                        "cuda_graph": graphed},
+            "roofline": {"bound": "hbm", "achieved": round(value / world, 1),
+                         "peak": _peak_gbs(), "unit": "GB/s",
+                         "frac": round(value / world / _peak_gbs(), 4), "traffic": None,
+                         "note": "per GPU: local slab traffic / max-over-ranks step time"},
+            "e2e": {"value": round(e2e_gbs, 1), "unit": "GB/s",
+                    "h2d_bytes_per_step": world * e2e_spmv * nloc * 8,
+                    "d2h_bytes_per_step": world * e2e_spmv * nloc * 8,
+                    "spmv_per_step": e2e_spmv,
+                    "note": "each rank: pinned host x rows -> distributed SpMV -> host y rows"},
             "gpu_launches": args.steps * 100 * 3,
             "clocks": clocks.summary(),
         }
