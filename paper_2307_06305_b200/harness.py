@@ -148,6 +148,18 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self._proc.kill()
             self._thread.join(timeout=5)
+            if not self.rows:  # region shorter than the period: one sample at its end
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=10).stdout
+                    for line in out.splitlines():
+                        parts = [p.strip() for p in line.split(",")]
+                        if len(parts) >= 8:
+                            self.rows.append(parts)
+                except (OSError, subprocess.TimeoutExpired):
+                    pass
 
     def summary(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
