@@ -16,7 +16,8 @@ from .errors import DeviceError, NativeLibraryMissing
 # DACSR_LIB=checked selects the bounds-checked build (tests only)
 _LIB_NAME = ("libdacsr_b200_checked.so" if os.environ.get("DACSR_LIB") == "checked"
              else "libdacsr_b200.so")
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", _LIB_NAME)
+LIB_PATH = os.environ.get("DACSR_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", _LIB_NAME)  # DACSR_LIB_PATH: A/B builds
 
 # dtype / kind / order / variant codes (dacsr_b200.h)
 I8, I16, I32, I64, F32, F64 = range(6)

@@ -555,8 +555,11 @@ __device__ __forceinline__ bool chunk_fits(IT first, IT last, int vcap, int alig
 
 // 64 registers (4 CTAs/SM): measured faster than 48 registers at 5 CTAs/SM
 // (C2: 33.5 vs 39.0 us) — the gather batch needs the registers for ILP.
+#ifndef DACSR_WSTREAM_MINB
+#define DACSR_WSTREAM_MINB 4
+#endif
 template <int KIND, class RP, class CI, class VT, int ORDER, int RPL>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, DACSR_WSTREAM_MINB)
     wstream_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re, int64_t nnz,
                    const int64_t* complex_list, int64_t n_complex, int side_ctas, int vcap) {
   using WC = WarpChunk<RP, CI, VT>;
