@@ -93,3 +93,28 @@ def test_c5_full_size_sampled(cuda):
             acc = acc + v * xc
         assert acc == float(y[r].item()), r
     del xs
+
+
+def test_nnz_above_2_31_int64_rowptr(cuda):
+    """Maximum-size edge: a C5-shaped matrix with nnz > 2^31 (Poisson(8.05)),
+    so rowptr must be int64 on the device; sampled rows vs the oracle."""
+    n, b, lam, kmax, seed = 1 << 28, 32767, 8.05, 32, 77
+    arr = banded_arrays(n, b, lam, kmax, seed, cuda, kinds=("da",))
+    assert arr["nnz"] > 2**31 and arr["rowptr"].dtype == torch.int64
+    dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"])
+    x = normal_vector(n, 5, cuda)
+    cdf, table = poisson_cdf(lam, kmax), normal_table()
+    rng = np.random.default_rng(2)
+    rows = np.concatenate([[0, n - 1, n // 2], rng.integers(n - (1 << 20), n, 40),
+                           rng.integers(0, n, 40)])
+    for kernel in ("wstream", "rowblock"):
+        y = torch.empty(n, dtype=torch.float64, device=cuda)
+        dm.spmv_into(x, y, 1.0, 0.0, kernel, 0)
+        for r in rows.tolist():
+            offs = oracle.gen_row(n, b, kmax, seed, cdf, r)
+            acc = 0.0
+            for o in offs.tolist():
+                xv = oracle.gen_normal(5, r + o, r + o + 1, table)[0]
+                acc = acc + oracle.gen_value(b, seed, r, o, table) * xv
+            assert acc == float(y[r].item()), (kernel, r)
+        del y
