@@ -158,6 +158,17 @@ int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t varian
                int32_t order, const void* x, int64_t x_offset, void* y, double alpha,
                double beta, int64_t row_start, int64_t row_end, void* stream);
 
+/* spmv with HOST x / y, copies overlapped with the kernels: rows split into
+ * the row ranges of plans[0..npieces) (ascending, covering the rows); piece
+ * p needs x[0, min(ncols, row_end_p + w)) with w the bandwidth (max |col -
+ * row|).  x_dev / y_dev are caller-owned device buffers of ncols / nrows
+ * values; the three streams carry H2D copies, kernels and D2H copies.
+ * Blocks until y_host is complete.  Host buffers should be pinned. */
+int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans, int32_t npieces,
+                             int32_t variant, int32_t order, const void* x_host, void* y_host,
+                             void* x_dev, void* y_dev, double alpha, double beta, int64_t w,
+                             void* s_h2d, void* s_comp, void* s_d2h);
+
 /* The reference's alpha == 0 short-cut (spmv/__init__.py:150-156):
  * y = 0 if beta == 0, y = (T)((double)beta * y) if beta not in {0, 1}. */
 int dacsr_scale(void* y, int32_t values_dtype, int64_t n, double beta, void* stream);

@@ -93,6 +93,8 @@ _SIGNATURES = {
     "dacsr_spmv": ([_P(Matrix), _P(Plan), _i32, _i32, _vp, _i64, _vp, _d, _d, _i64, _i64, _vp],
                    ctypes.c_int),
     "dacsr_scale": ([_vp, _i32, _i64, _d, _vp], ctypes.c_int),
+    "dacsr_spmv_host_streamed": ([_P(Matrix), _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _d, _d,
+                                  _i64, _vp, _vp, _vp], ctypes.c_int),
     "dacsr_sumsq_chunks": ([_vp, _i32, _i64, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_sum_ordered": ([_vp, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_bandwidth": ([_P(Matrix), _vp, _vp], ctypes.c_int),

@@ -1059,6 +1059,80 @@ int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t varian
   return DACSR_ERR_DTYPE;
 }
 
+// Host-buffer SpMV with the copies overlapped (see hostpath.py): rows are
+// split into the plans' row ranges; piece p needs x[0, min(ncols, r1_p + w))
+// (w = bandwidth).  h2d: the x prefix not yet sent (+ the y piece if
+// beta != 0); comp: waits for it, runs the piece; d2h: waits for the piece,
+// copies its y rows back.  Blocks until y_host is complete.
+int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans, int32_t npieces,
+                             int32_t variant, int32_t order, const void* x_host, void* y_host,
+                             void* x_dev, void* y_dev, double alpha, double beta, int64_t w,
+                             void* s_h2d, void* s_comp, void* s_d2h) {
+  if (!a || !plans || npieces <= 0 || npieces > 64 || !x_host || !y_host || !x_dev || !y_dev ||
+      w < 0)
+    return DACSR_ERR_ARG;
+  static const int kBytes[6] = {1, 2, 4, 8, 4, 8};
+  if (a->values_dtype != DACSR_F32 && a->values_dtype != DACSR_F64) return DACSR_ERR_DTYPE;
+  const size_t vb = kBytes[a->values_dtype];
+  auto h2d = static_cast<cudaStream_t>(s_h2d), comp = static_cast<cudaStream_t>(s_comp),
+       d2h = static_cast<cudaStream_t>(s_d2h);
+  cudaEvent_t ev[128];
+  int nev = 0;
+  auto fail = [&](const char* what, cudaError_t e) {
+    set_last_error(what, e);
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+    return DACSR_ERR_CUDA;
+  };
+  for (int i = 0; i < 2 * npieces; ++i) {
+    cudaError_t e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return fail("streamed event", e);
+    ++nev;
+  }
+  const char* xh = static_cast<const char*>(x_host);
+  char* yh = static_cast<char*>(y_host);
+  char* xd = static_cast<char*>(x_dev);
+  char* yd = static_cast<char*>(y_dev);
+  int64_t sent = 0;
+  cudaError_t e;
+  for (int p = 0; p < npieces; ++p) {
+    const int64_t r0 = plans[p].row_start, r1 = plans[p].row_end;
+    const int64_t hi = std::min<int64_t>(a->ncols, r1 + w);
+    if (hi > sent) {
+      e = cudaMemcpyAsync(xd + sent * vb, xh + sent * vb, (hi - sent) * vb,
+                          cudaMemcpyHostToDevice, h2d);
+      if (e != cudaSuccess) return fail("streamed x copy", e);
+      sent = hi;
+    }
+    if (beta != 0.0 && r1 > r0) {
+      e = cudaMemcpyAsync(yd + r0 * vb, yh + r0 * vb, (r1 - r0) * vb, cudaMemcpyHostToDevice, h2d);
+      if (e != cudaSuccess) return fail("streamed y copy in", e);
+    }
+    if ((e = cudaEventRecord(ev[2 * p], h2d)) != cudaSuccess) return fail("event", e);
+    if ((e = cudaStreamWaitEvent(comp, ev[2 * p], 0)) != cudaSuccess) return fail("wait", e);
+    if (r1 > r0) {
+      const int rc = dacsr_spmv(a, &plans[p], variant, order, x_dev, 0, y_dev, alpha, beta, r0, r1,
+                                s_comp);
+      if (rc) {
+        for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+        return rc;
+      }
+    }
+    if ((e = cudaEventRecord(ev[2 * p + 1], comp)) != cudaSuccess) return fail("event", e);
+    if ((e = cudaStreamWaitEvent(d2h, ev[2 * p + 1], 0)) != cudaSuccess) return fail("wait", e);
+    if (r1 > r0) {
+      e = cudaMemcpyAsync(yh + r0 * vb, yd + r0 * vb, (r1 - r0) * vb, cudaMemcpyDeviceToHost, d2h);
+      if (e != cudaSuccess) return fail("streamed y copy out", e);
+    }
+  }
+  e = cudaStreamSynchronize(d2h);
+  for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+  if (e != cudaSuccess) {
+    set_last_error("streamed sync", e);
+    return DACSR_ERR_CUDA;
+  }
+  return DACSR_OK;
+}
+
 // Reference-named kernels: the paper's layout (int32 rowptr; DA int16
 // offsets, CSR int32 colids), the named order, STAGED engine (no plan).
 #define DACSR_DEFINE_TYPED(KIND, KCODE, CI, CICODE, NAME, ORDER, VT, VCODE, VN)                 \

@@ -38,40 +38,43 @@ class StreamedHost:
         dev = dm.device
         self.x = torch.empty(max(dm.ncols, 1), dtype=dm.values.dtype, device=dev)
         self.y = torch.empty(max(n, 1), dtype=dm.values.dtype, device=dev)
+        self._plans = {}
         self.s_h2d = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev)
         self.s_d2h = torch.cuda.Stream(dev)
 
     def run(self, x_host, y_host, alpha, beta, kname, order):
+        """One C-ABI call issues every copy, event and kernel of the pipeline
+        (dacsr_spmv_host_streamed); Python only resolves the per-piece plans
+        once per (kernel, order)."""
+        import ctypes
+        from . import _native
+        key = (kname, order)
+        rec = self._plans.get(key)
+        if rec is None:
+            kernels = [kernel_for(v, kname, order) for v in self.views]
+            if len(set(kernels)) != 1:
+                kernels = ["staged"] * len(self.views)
+            k = kernels[0]
+            plans = (_native.Plan * len(self.views))()
+            for i, v in enumerate(self.views):
+                pl = v.plan_for(k)
+                if pl is None:  # plan-free kernel: row range only
+                    plans[i].row_start, plans[i].row_end = v.row_start, v.row_end
+                else:
+                    ctypes.memmove(ctypes.byref(plans[i]), ctypes.byref(pl), ctypes.sizeof(pl))
+            rec = (plans, _native.VARIANT_CODES[k])
+            self._plans[key] = rec
+        plans, code = rec
         dm = self.dm
-        xh = torch.from_numpy(x_host)
-        yh = torch.from_numpy(y_host)
-        pinned = xh.is_pinned() and yh.is_pinned()
         cur = torch.cuda.current_stream(dm.device)
         for s in (self.s_h2d, self.s_comp, self.s_d2h):
             s.wait_stream(cur)
-        sent = 0
-        for v in self.views:
-            hi = min(dm.ncols, v.row_end + self.w)  # columns of rows < row_end are < row_end + w
-            with torch.cuda.stream(self.s_h2d):
-                if hi > sent:
-                    self.x[sent:hi].copy_(xh[sent:hi], non_blocking=pinned)
-                    sent = hi
-                if beta != 0.0:
-                    self.y[v.row_start:v.row_end].copy_(yh[v.row_start:v.row_end],
-                                                        non_blocking=pinned)
-            ev_in = torch.cuda.Event()
-            ev_in.record(self.s_h2d)
-            self.s_comp.wait_event(ev_in)
-            k = kernel_for(v, kname, order)
-            v.spmv_into(self.x, self.y, alpha, beta, k, order, stream=self.s_comp)
-            ev_out = torch.cuda.Event()
-            ev_out.record(self.s_comp)
-            self.s_d2h.wait_event(ev_out)
-            with torch.cuda.stream(self.s_d2h):
-                yh[v.row_start:v.row_end].copy_(self.y[v.row_start:v.row_end],
-                                                non_blocking=pinned)
-        self.s_d2h.synchronize()
+        _native.check(_native.lib().dacsr_spmv_host_streamed(
+            ctypes.byref(dm.desc), plans, len(self.views), code, int(order),
+            x_host.ctypes.data, y_host.ctypes.data, self.x.data_ptr(), self.y.data_ptr(),
+            float(alpha), float(beta), int(self.w), self.s_h2d.cuda_stream,
+            self.s_comp.cuda_stream, self.s_d2h.cuda_stream), "dacsr_spmv_host_streamed")
         return y_host
 
 
