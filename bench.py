@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--variant", default="naive")
     ap.add_argument("--no-suite", action="store_true", help="skip the C1/C2-f32/C3/C4 lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--suite", default="c1,c2f32,c3,c4")
+    ap.add_argument("--suite", default="c1,c2f32,c2bf16,c3,c4")
     ap.add_argument("--distributed", action="store_true",
                     help="use the row-block/halo path even at one rank (plumbing check)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
@@ -287,6 +287,14 @@ def suite_builders():
         return host_pair(csr, uniform_x(csr.ncols, 1).astype(np.float32),
                          "3D 7-pt 128^3 f32 (113 MB DA)")
 
+    def c2bf16():
+        # width-lattice extension: bf16 values/x/y, f64 sums
+        csr = laplacian_3d(128)
+        mats = {k: DeviceMatrix.from_host(a).astype(torch.bfloat16)
+                for k, a in (("da", dg.to_dacsr(csr, 16)), ("csr", csr))}
+        x = torch.from_numpy(uniform_x(csr.ncols, 1)).to(dev).to(torch.bfloat16)
+        return mats, x, "3D 7-pt 128^3 bf16 values/x/y, f64 accumulate (75 MB DA)"
+
     def c3():
         m = banded_device("c3", dev)
         return m, normal_vector(m["da"].ncols, 17, dev), "random banded n=2^24 b=32767 Poisson(16)"
@@ -298,7 +306,7 @@ def suite_builders():
                          f"{info['bandwidth_rcm']}) + Pareto(1.5) skew rows, max row "
                          f"{int(np.diff(a.rowptr).max())}")
 
-    return {"c1": c1, "c2f32": c2f32, "c3": c3, "c4": c4}
+    return {"c1": c1, "c2f32": c2f32, "c2bf16": c2bf16, "c3": c3, "c4": c4}
 
 
 def run_c5(args, world, rank, local):

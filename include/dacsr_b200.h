@@ -41,6 +41,11 @@ enum {
 
 /* ---- dtype, kind, order, variant codes ---------------------------------- */
 enum { DACSR_I8 = 0, DACSR_I16 = 1, DACSR_I32 = 2, DACSR_I64 = 3, DACSR_F32 = 4, DACSR_F64 = 5 };
+/* 16-bit values (extension along model.py:21-74's width lattice; the
+ * reference kernels stop at f32): values, x and y in binary16 / bfloat16,
+ * products exact in f32, f64 accumulation in the selected order, one
+ * rounding on the store. */
+enum { DACSR_F16 = 6, DACSR_BF16 = 7 };
 enum { DACSR_KIND_CSR = 0, DACSR_KIND_DA = 1 };
 
 /* Summation order inside a row.  NAIVE/MACC3/STRIP4 reproduce the

@@ -29,12 +29,13 @@
  * Pinned by tests/test_oracle.py against the fixtures in tests/golden, which the
  * reference itself generated (tests/golden/make_golden.py).
  */
+#include <math.h>
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
-enum { ORC_I8 = 0, ORC_I16 = 1, ORC_I32 = 2, ORC_I64 = 3, ORC_F32 = 4, ORC_F64 = 5 };
+enum { ORC_I8 = 0, ORC_I16 = 1, ORC_I32 = 2, ORC_I64 = 3, ORC_F32 = 4, ORC_F64 = 5, ORC_F16 = 6, ORC_BF16 = 7 };
 enum { ORC_NAIVE = 0, ORC_MACC3 = 1, ORC_STRIP4 = 2 };
 enum { ORC_CSR = 0, ORC_DA = 1 };
 
@@ -43,62 +44,130 @@ enum { ORC_CSR = 0, ORC_DA = 1 };
 #define COLUMN_CSR(r, c) ((int64_t)(c))
 #define COLUMN_DA(r, c) ((int64_t)(r) + (int64_t)(c))
 
-/* one product, rounded like numba: f64*f64 -> f64, f32*f32 -> f32 */
-#define PROD(V, X) ((V) * (X))
+/* Per value type: storage type T, product P (as the double that is summed),
+ * load-to-double L, store-with-one-rounding S.
+ *   f64: product rounded in f64;  f32: product rounded to f32, widened
+ *   (numba: f32*f32 -> f32, acc float64);  f16/bf16 (extension, no reference
+ *   kernel): the f32 product of two 16-bit significands is exact, the sum is
+ *   f64 in the same order, one rounding to 16 bits on the store. */
+static float h16_to_f32(uint16_t h) {
+  const int e = (h >> 10) & 31, m = h & 1023;
+  float v;
+  if (e == 0) v = ldexpf((float)m, -24);
+  else if (e == 31) v = m ? NAN : INFINITY;
+  else v = ldexpf((float)(1024 + m), e - 25);
+  return (h & 0x8000) ? -v : v;
+}
+static float b16_to_f32(uint16_t h) {
+  uint32_t u = (uint32_t)h << 16;
+  float v;
+  memcpy(&v, &u, 4);
+  return v;
+}
+/* round a double to a 16-bit binary format with p significand bits (incl.
+ * the hidden one), exponent range [emin, emax] and bias ebias: round to
+ * nearest even, directly from the double (no f32 detour) */
+static uint16_t round_bits(double d, int p, int emin, int ebias, int emax) {
+  const uint16_t sign = signbit(d) ? 0x8000 : 0;
+  const int mbits = p - 1;
+  if (isnan(d)) return sign | (uint16_t)(((2 * ebias + 1) << mbits) | (1 << (mbits - 1)));
+  const double a = fabs(d);
+  if (a == 0.0) return sign;
+  if (isinf(a)) return sign | (uint16_t)((2 * ebias + 1) << mbits);
+  int e2;
+  frexp(a, &e2);
+  int E = e2 - 1; /* a in [2^E, 2^(E+1)) */
+  if (E < emin) E = emin;
+  double q = rint(ldexp(a, mbits - E)); /* significand in units of 2^(E-mbits) */
+  if (q >= ldexp(1.0, p)) { q = ldexp(q, -1); E += 1; } /* q == 2^p exactly: renormalise */
+  if (E > emax) return sign | (uint16_t)((2 * ebias + 1) << mbits); /* inf */
+  const uint32_t qi = (uint32_t)q;
+  if (qi < (1u << mbits)) return sign | (uint16_t)qi; /* subnormal (E == emin) */
+  return sign | (uint16_t)(((uint32_t)(E + ebias) << mbits) | (qi - (1u << mbits)));
+}
+static uint16_t f64_to_h16(double d) { return round_bits(d, 11, -14, 15, 15); }
+static uint16_t f64_to_b16(double d) { return round_bits(d, 8, -126, 127, 127); }
 
-#define DEFINE_ROWS(NAME, RP, CI, VT, COLUMN)                                          \
-  static void NAME##_naive(const RP* rp, const CI* ci, const VT* v, const VT* x,       \
-                           VT* y, double alpha, double beta, int64_t rs, int64_t re) {  \
+#define f64_T double
+#define f64_P(V, X) ((V) * (X))
+#define f64_L(Y) ((double)(Y))
+#define f64_S(D) (D)
+#define f32_T float
+#define f32_P(V, X) ((double)((V) * (X)))
+#define f32_L(Y) ((double)(Y))
+#define f32_S(D) ((float)(D))
+#define f16_T uint16_t
+#define f16_P(V, X) ((double)(h16_to_f32(V) * h16_to_f32(X)))
+#define f16_L(Y) ((double)h16_to_f32(Y))
+#define f16_S(D) f64_to_h16(D)
+#define bf16_T uint16_t
+#define bf16_P(V, X) ((double)(b16_to_f32(V) * b16_to_f32(X)))
+#define bf16_L(Y) ((double)b16_to_f32(Y))
+#define bf16_S(D) f64_to_b16(D)
+
+#define EPI(VN, r, acc) \
+  y[r] = VN##_S(beta == 0.0 ? alpha * (acc) : alpha * (acc) + beta * VN##_L(y[r]))
+
+#define DEFINE_ROWS(NAME, RP, CI, VN, COLUMN)                                          \
+  static void NAME##_naive(const RP* rp, const CI* ci, const VN##_T* v,                \
+                           const VN##_T* x, VN##_T* y, double alpha, double beta,      \
+                           int64_t rs, int64_t re) {                                   \
     for (int64_t r = rs; r < re; ++r) {                                                \
       double acc = 0.0;                                                                \
       for (int64_t i = (int64_t)rp[r]; i < (int64_t)rp[r + 1]; ++i)                    \
-        acc += PROD(v[i], x[COLUMN(r, ci[i])]);                                        \
-      y[r] = (VT)(beta == 0.0 ? alpha * acc : alpha * acc + beta * (double)y[r]);      \
+        acc += VN##_P(v[i], x[COLUMN(r, ci[i])]);                                      \
+      EPI(VN, r, acc);                                                                 \
     }                                                                                  \
   }                                                                                    \
-  static void NAME##_macc3(const RP* rp, const CI* ci, const VT* v, const VT* x,       \
-                           VT* y, double alpha, double beta, int64_t rs, int64_t re) {  \
+  static void NAME##_macc3(const RP* rp, const CI* ci, const VN##_T* v,                \
+                           const VN##_T* x, VN##_T* y, double alpha, double beta,      \
+                           int64_t rs, int64_t re) {                                   \
     for (int64_t r = rs; r < re; ++r) {                                                \
       int64_t i = (int64_t)rp[r], e = (int64_t)rp[r + 1];                              \
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;                                             \
       for (; i + 3 <= e; i += 3) {                                                     \
-        a0 += PROD(v[i], x[COLUMN(r, ci[i])]);                                         \
-        a1 += PROD(v[i + 1], x[COLUMN(r, ci[i + 1])]);                                 \
-        a2 += PROD(v[i + 2], x[COLUMN(r, ci[i + 2])]);                                 \
+        a0 += VN##_P(v[i], x[COLUMN(r, ci[i])]);                                       \
+        a1 += VN##_P(v[i + 1], x[COLUMN(r, ci[i + 1])]);                               \
+        a2 += VN##_P(v[i + 2], x[COLUMN(r, ci[i + 2])]);                               \
       }                                                                                \
-      if (i < e) a0 += PROD(v[i], x[COLUMN(r, ci[i])]);                                \
-      if (i + 1 < e) a1 += PROD(v[i + 1], x[COLUMN(r, ci[i + 1])]);                    \
+      if (i < e) a0 += VN##_P(v[i], x[COLUMN(r, ci[i])]);                              \
+      if (i + 1 < e) a1 += VN##_P(v[i + 1], x[COLUMN(r, ci[i + 1])]);                  \
       double acc = (a0 + a1) + a2;                                                     \
-      y[r] = (VT)(beta == 0.0 ? alpha * acc : alpha * acc + beta * (double)y[r]);      \
+      EPI(VN, r, acc);                                                                 \
     }                                                                                  \
   }                                                                                    \
-  static void NAME##_strip4(const RP* rp, const CI* ci, const VT* v, const VT* x,      \
-                            VT* y, double alpha, double beta, int64_t rs, int64_t re) { \
+  static void NAME##_strip4(const RP* rp, const CI* ci, const VN##_T* v,               \
+                            const VN##_T* x, VN##_T* y, double alpha, double beta,     \
+                            int64_t rs, int64_t re) {                                  \
     for (int64_t r = rs; r < re; ++r) {                                                \
       int64_t i = (int64_t)rp[r], e = (int64_t)rp[r + 1];                              \
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;                                   \
       for (; i + 4 <= e; i += 4) {                                                     \
-        a0 += PROD(v[i], x[COLUMN(r, ci[i])]);                                         \
-        a1 += PROD(v[i + 1], x[COLUMN(r, ci[i + 1])]);                                 \
-        a2 += PROD(v[i + 2], x[COLUMN(r, ci[i + 2])]);                                 \
-        a3 += PROD(v[i + 3], x[COLUMN(r, ci[i + 3])]);                                 \
+        a0 += VN##_P(v[i], x[COLUMN(r, ci[i])]);                                       \
+        a1 += VN##_P(v[i + 1], x[COLUMN(r, ci[i + 1])]);                               \
+        a2 += VN##_P(v[i + 2], x[COLUMN(r, ci[i + 2])]);                               \
+        a3 += VN##_P(v[i + 3], x[COLUMN(r, ci[i + 3])]);                               \
       }                                                                                \
       double acc = (a0 + a1) + (a2 + a3);                                              \
       double tail = 0.0;                                                               \
-      for (; i < e; ++i) tail += PROD(v[i], x[COLUMN(r, ci[i])]);                      \
+      for (; i < e; ++i) tail += VN##_P(v[i], x[COLUMN(r, ci[i])]);                    \
       acc = acc + tail;                                                                \
-      y[r] = (VT)(beta == 0.0 ? alpha * acc : alpha * acc + beta * (double)y[r]);      \
+      EPI(VN, r, acc);                                                                 \
     }                                                                                  \
   }
 
 typedef void (*rows_fn)(const void*, const void*, const void*, const void*, void*, double,
                         double, int64_t, int64_t);
 
-#define DEFINE_KIND_VT(RPN, RP, CIN, CI)                                       \
-  DEFINE_ROWS(csr_##RPN##_##CIN##_f64, RP, CI, double, COLUMN_CSR)            \
-  DEFINE_ROWS(csr_##RPN##_##CIN##_f32, RP, CI, float, COLUMN_CSR)             \
-  DEFINE_ROWS(da_##RPN##_##CIN##_f64, RP, CI, double, COLUMN_DA)              \
-  DEFINE_ROWS(da_##RPN##_##CIN##_f32, RP, CI, float, COLUMN_DA)
+#define DEFINE_KIND_VT(RPN, RP, CIN, CI)                                \
+  DEFINE_ROWS(csr_##RPN##_##CIN##_f64, RP, CI, f64, COLUMN_CSR)        \
+  DEFINE_ROWS(csr_##RPN##_##CIN##_f32, RP, CI, f32, COLUMN_CSR)        \
+  DEFINE_ROWS(csr_##RPN##_##CIN##_f16, RP, CI, f16, COLUMN_CSR)        \
+  DEFINE_ROWS(csr_##RPN##_##CIN##_bf16, RP, CI, bf16, COLUMN_CSR)      \
+  DEFINE_ROWS(da_##RPN##_##CIN##_f64, RP, CI, f64, COLUMN_DA)          \
+  DEFINE_ROWS(da_##RPN##_##CIN##_f32, RP, CI, f32, COLUMN_DA)          \
+  DEFINE_ROWS(da_##RPN##_##CIN##_f16, RP, CI, f16, COLUMN_DA)          \
+  DEFINE_ROWS(da_##RPN##_##CIN##_bf16, RP, CI, bf16, COLUMN_DA)
 
 #define DEFINE_RP(RPN, RP)               \
   DEFINE_KIND_VT(RPN, RP, i8, int8_t)    \
@@ -109,23 +178,24 @@ typedef void (*rows_fn)(const void*, const void*, const void*, const void*, void
 DEFINE_RP(p32, int32_t)
 DEFINE_RP(p64, int64_t)
 
-/* table [kind][rp 0=i32,1=i64][ci 0..3][vt 0=f32,1=f64][order] */
+/* table [kind][rp 0=i32,1=i64][ci 0..3][vt 0=f32,1=f64,2=f16,3=bf16][order] */
 #define ENTRY(K, RPN, CIN, VTN) \
   {(rows_fn)K##_##RPN##_##CIN##_##VTN##_naive, (rows_fn)K##_##RPN##_##CIN##_##VTN##_macc3, \
    (rows_fn)K##_##RPN##_##CIN##_##VTN##_strip4}
-#define ENTRY_VT(K, RPN, CIN) {ENTRY(K, RPN, CIN, f32), ENTRY(K, RPN, CIN, f64)}
+#define ENTRY_VT(K, RPN, CIN) \
+  {ENTRY(K, RPN, CIN, f32), ENTRY(K, RPN, CIN, f64), ENTRY(K, RPN, CIN, f16), ENTRY(K, RPN, CIN, bf16)}
 #define ENTRY_CI(K, RPN) \
   {ENTRY_VT(K, RPN, i8), ENTRY_VT(K, RPN, i16), ENTRY_VT(K, RPN, i32), ENTRY_VT(K, RPN, i64)}
 #define ENTRY_RP(K) {ENTRY_CI(K, p32), ENTRY_CI(K, p64)}
 
-static const rows_fn TABLE[2][2][4][2][3] = {ENTRY_RP(csr), ENTRY_RP(da)};
+static const rows_fn TABLE[2][2][4][4][3] = {ENTRY_RP(csr), ENTRY_RP(da)};
 
 static rows_fn lookup(int kind, int order, int rp_dt, int ci_dt, int val_dt) {
   if (kind < 0 || kind > 1 || order < 0 || order > 2) return NULL;
   if (rp_dt != ORC_I32 && rp_dt != ORC_I64) return NULL;
   if (ci_dt < ORC_I8 || ci_dt > ORC_I64) return NULL;
-  if (val_dt != ORC_F32 && val_dt != ORC_F64) return NULL;
-  return TABLE[kind][rp_dt == ORC_I64][ci_dt][val_dt == ORC_F64][order];
+  if (val_dt < ORC_F32 || val_dt > ORC_BF16) return NULL;
+  return TABLE[kind][rp_dt == ORC_I64][ci_dt][val_dt - ORC_F32][order];
 }
 
 int orc_spmv(int kind, int order, int rp_dt, int ci_dt, int val_dt, const void* rowptr,
@@ -135,6 +205,14 @@ int orc_spmv(int kind, int order, int rp_dt, int ci_dt, int val_dt, const void* 
   if (!f) return 1;
   f(rowptr, colids, values, x, y, alpha, beta, row_start, row_end);
   return 0;
+}
+
+/* 16-bit conversions (tests): f64 -> bits with one RNE rounding, bits -> f64 */
+void orc_to_half_bits(const double* in, uint16_t* out, int64_t n, int bf16) {
+  for (int64_t i = 0; i < n; ++i) out[i] = bf16 ? f64_to_b16(in[i]) : f64_to_h16(in[i]);
+}
+void orc_from_half_bits(const uint16_t* in, double* out, int64_t n, int bf16) {
+  for (int64_t i = 0; i < n; ++i) out[i] = bf16 ? b16_to_f32(in[i]) : h16_to_f32(in[i]);
 }
 
 /* ------------------------------------------------------------ row_blocks */

@@ -33,7 +33,9 @@ LIB_PATH = os.path.join(HERE, "liboracle.so")
 
 ORDERS = {"naive": 0, "shifted_base": 0, "multi_accumulator_3": 1, "strip_mined_4": 2}
 _DT = {np.dtype(np.int8): 0, np.dtype(np.int16): 1, np.dtype(np.int32): 2,
-       np.dtype(np.int64): 3, np.dtype(np.float32): 4, np.dtype(np.float64): 5}
+       np.dtype(np.int64): 3, np.dtype(np.float32): 4, np.dtype(np.float64): 5,
+       np.dtype(np.float16): 6}
+BF16 = 7  # bfloat16 arrays travel as uint16 bit patterns (numpy has no bf16)
 
 _lib = None
 
@@ -54,6 +56,8 @@ def lib():
         L.orc_spmv.argtypes = [i32] * 5 + [vp] * 5 + [d, d, i64, i64]
         L.orc_spmv_parallel.argtypes = [i32] * 5 + [vp] * 5 + [d, d, i64, i32]
         L.orc_row_blocks.argtypes = [vp, i32, i64, i64, vp]
+        L.orc_to_half_bits.argtypes = [vp, vp, i64, i32]
+        L.orc_from_half_bits.argtypes = [vp, vp, i64, i32]
         L.orc_rcm.argtypes = [i64, vp, vp, vp]
         L.orc_gen_row.argtypes = [i64, i64, i32, u64, vp, i64, vp]
         L.orc_gen_value.argtypes = [i64, u64, i64, ctypes.c_int32, vp]
@@ -77,13 +81,31 @@ def _rowptr_arg(rowptr):
     return rp
 
 
+def to_half_bits(a, bf16=False):
+    """float64 array -> 16-bit patterns (binary16 or bfloat16), one RNE rounding."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    out = np.empty(a.shape, np.uint16)
+    lib().orc_to_half_bits(_p(a), _p(out), a.size, int(bf16))
+    return out
+
+
+def from_half_bits(bits, bf16=False):
+    """16-bit patterns -> float64 (exact)."""
+    b = np.ascontiguousarray(bits).view(np.uint16)
+    out = np.empty(b.shape, np.float64)
+    lib().orc_from_half_bits(_p(b), _p(out), b.size, int(bf16))
+    return out
+
+
 def spmv_kernel(kind, rowptr, colids, values, x, y, alpha, beta, order="naive",
-                row_start=0, row_end=None, threads=1, x_offset=0):
+                row_start=0, row_end=None, threads=1, x_offset=0, bf16=False):
     """Run the restated reference kernel in place on ``y``.
 
     ``kind`` is "csr" or "da"; ``threads > 1`` is ParallelRowBlock(threads).
     ``x_offset`` shifts x addressing (x[col + x_offset]) for rank-local halo
-    buffers; the reference kernel is the x_offset == 0 case.
+    buffers; the reference kernel is the x_offset == 0 case.  16-bit values
+    (an extension, no reference kernel): float16 arrays, or with ``bf16``
+    uint16 arrays holding bfloat16 bit patterns.
     """
     rp = _rowptr_arg(rowptr)
     ci = np.ascontiguousarray(colids)
@@ -94,7 +116,8 @@ def spmv_kernel(kind, rowptr, colids, values, x, y, alpha, beta, order="naive",
     row_end = nrows if row_end is None else row_end
     k = {"csr": 0, "da": 1}[kind]
     xp = ctypes.c_void_p((xx.ctypes.data or 0) + int(x_offset) * xx.itemsize)
-    args = (k, ORDERS[order], _DT[rp.dtype], _DT[ci.dtype], _DT[v.dtype],
+    vcode = BF16 if bf16 else _DT[v.dtype]
+    args = (k, ORDERS[order], _DT[rp.dtype], _DT[ci.dtype], vcode,
             _p(rp), _p(ci), _p(v), xp, _p(y), float(alpha), float(beta))
     if threads == 1:
         rc = lib().orc_spmv(*args, row_start, row_end)

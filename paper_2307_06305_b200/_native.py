@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("DACSR_LIB_PATH") or os.path.join(
 
 # dtype / kind / order / variant codes (dacsr_b200.h)
 I8, I16, I32, I64, F32, F64 = range(6)
+F16, BF16 = 6, 7  # 16-bit values (extension; see include/dacsr_b200.h)
 KIND_CSR, KIND_DA = 0, 1
 ORDER_NAIVE, ORDER_MACC3, ORDER_STRIP4, ORDER_TREE = range(4)
 VARIANT_CODES = {
@@ -32,7 +33,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported dtype", 3: "unknown va
 ANALYZE_SCRATCH = 64
 
 _NP_CODE = {"int8": I8, "int16": I16, "int32": I32, "int64": I64, "float32": F32,
-            "float64": F64}
+            "float64": F64, "float16": F16, "bfloat16": BF16}
 
 
 def dtype_code(dtype):

@@ -84,7 +84,7 @@ __global__ void scale_kernel(VT* y, int64_t n, double beta) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += stride) {
-    if (beta == 0.0) y[i] = VT(0);
+    if (beta == 0.0) store_rounded(y + i, 0.0);
     else store_rounded(y + i, __dmul_rn(beta, to_f64(y[i])));
   }
 }
@@ -226,8 +226,8 @@ int dacsr_analyze(const dacsr_matrix_t* a, int64_t rs, int64_t re, void* scratch
 }
 
 int32_t dacsr_plan_default_cap(const dacsr_stats_t* s, int32_t values_dtype, int32_t colids_dtype) {
-  static const int kBytes[6] = {1, 2, 4, 8, 4, 8};
-  if (!s || values_dtype < 0 || values_dtype > 5 || colids_dtype < 0 || colids_dtype > 5) return 2048;
+  static const int kBytes[8] = {1, 2, 4, 8, 4, 8, 2, 2};
+  if (!s || values_dtype < 0 || values_dtype > 7 || colids_dtype < 0 || colids_dtype > 5) return 2048;
   const int per = kBytes[values_dtype] + kBytes[colids_dtype];
   // about 0.9 rows per thread of a 512-thread CTA, >= 2 stages in 100 KiB
   double cap = 0.9 * 512.0 * std::max(s->mean_len, 1.0);
@@ -278,6 +278,9 @@ int dacsr_scale(void* y, int32_t vdt, int64_t n, double beta, void* stream) {
   const int g = grid_for(n, 256);
   if (vdt == DACSR_F64) scale_kernel<double><<<g, 256, 0, st>>>(static_cast<double*>(y), n, beta);
   else if (vdt == DACSR_F32) scale_kernel<float><<<g, 256, 0, st>>>(static_cast<float*>(y), n, beta);
+  else if (vdt == DACSR_F16) scale_kernel<__half><<<g, 256, 0, st>>>(static_cast<__half*>(y), n, beta);
+  else if (vdt == DACSR_BF16)
+    scale_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<__nv_bfloat16*>(y), n, beta);
   else return DACSR_ERR_DTYPE;
   return check_launch("scale_kernel");
 }

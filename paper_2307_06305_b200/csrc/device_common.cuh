@@ -3,6 +3,8 @@
 // reference's rounding rules, and error plumbing for the C ABI.
 #pragma once
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -88,10 +90,28 @@ __device__ __forceinline__ double product(float v, float x) {
   return static_cast<double>(__fmul_rn(v, x));
 }
 
+// 16-bit data: the f32 product of two 16-bit significands is exact
+// (11+11 <= 24, 8+8 <= 24 bits), so the f64 sum sees the exact product.
+__device__ __forceinline__ double product(__half v, __half x) {
+  return static_cast<double>(__fmul_rn(__half2float(v), __half2float(x)));
+}
+__device__ __forceinline__ double product(__nv_bfloat16 v, __nv_bfloat16 x) {
+  return static_cast<double>(__fmul_rn(__bfloat162float(v), __bfloat162float(x)));
+}
+
 __device__ __forceinline__ double to_f64(double v) { return v; }
 __device__ __forceinline__ double to_f64(float v) { return static_cast<double>(v); }
+__device__ __forceinline__ double to_f64(__half v) { return static_cast<double>(__half2float(v)); }
+__device__ __forceinline__ double to_f64(__nv_bfloat16 v) {
+  return static_cast<double>(__bfloat162float(v));
+}
 __device__ __forceinline__ void store_rounded(double* p, double v) { *p = v; }
 __device__ __forceinline__ void store_rounded(float* p, double v) { *p = __double2float_rn(v); }
+// one rounding f64 -> 16 bit (round to nearest even, no detour through f32)
+__device__ __forceinline__ void store_rounded(__half* p, double v) { *p = __double2half(v); }
+__device__ __forceinline__ void store_rounded(__nv_bfloat16* p, double v) {
+  *p = __double2bfloat16(v);
+}
 
 // y[r] = alpha*acc (+ beta*y[r] iff beta != 0); y is not read when beta == 0.
 template <class VT>

@@ -23,20 +23,9 @@
 // Column of entry i in row r: CSR colids[i]; DA r + colids[i] (the shifted
 // base of PAPER.md Snippet 2); plus x_offset for rank-local halo buffers.
 
-#include <algorithm>
-#include <cstdio>
-#include <cstring>
-#include <mutex>
-
-#include "device_common.cuh"
+#include "spmv_kernels.cuh"
 
 namespace dacsr {
-
-constexpr int kMaxThreads = 512;
-constexpr int kMaxStages = 4;
-constexpr int kMaxLong = 64;      // rows > long_len starting in one chunk (<= cap/long_len+1)
-constexpr int kLongChunk = 512;   // products per cooperative round (x2 buffers)
-constexpr int kScratchBytes = 2 * kLongChunk * 8;
 
 // ------------------------------------------------------------- error state
 namespace {
@@ -57,923 +46,6 @@ int check_launch(const char* what) {
   return DACSR_OK;
 }
 
-__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
-
-// ------------------------------------------------------------- kernel args
-template <int KIND, class RP, class CI, class VT>
-struct Mat {
-  const RP* __restrict__ rp;
-  const CI* __restrict__ ci;
-  const VT* __restrict__ v;
-  const VT* __restrict__ x;
-  VT* __restrict__ y;
-  int64_t xoff;
-  int64_t nrows, ncols, nnz;  // bounds for the checked build
-  __device__ __forceinline__ int64_t col(int64_t r, CI c) const {
-    return (KIND == DACSR_KIND_DA ? r + static_cast<int64_t>(c) : static_cast<int64_t>(c)) +
-           xoff;
-  }
-  // entry i of row r: checked build verifies i, the row and the column
-  __device__ __forceinline__ void check(int64_t r, int64_t i, CI c) const {
-    DACSR_CHECK(r >= 0 && r < nrows);
-    DACSR_CHECK(i >= 0 && i < nnz);
-    DACSR_CHECK(col(r, c) - xoff >= 0 && col(r, c) - xoff < ncols);
-    (void)r; (void)i; (void)c;
-  }
-  __device__ __forceinline__ double prod_global(int64_t r, int64_t i) const {
-    const CI c = ldg(ci + i);
-    check(r, i, c);
-    return product(ldg(v + i), ldg(x + col(r, c)));
-  }
-};
-
-struct Scal {
-  double alpha, beta;
-  int order;
-  int64_t long_len;
-};
-
-struct Chunks {
-  const int64_t* block_rows;
-  int64_t base, end, nblocks;
-  int cap, stages;
-};
-
-// --------------------------------------------------- block reduce (TREE)
-__device__ __forceinline__ double block_sum_tree(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (warp == 0) {
-    t = lane < nw ? red[lane] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
-  }
-  __syncthreads();
-  return t;  // valid in thread 0
-}
-
-// Entry i of row r as seen by a CTA whose chunk [lo, hi) sits in smem.
-template <int KIND, class RP, class CI, class VT>
-struct StagedGet {
-  const Mat<KIND, RP, CI, VT>& m;
-  const VT* sv;
-  const CI* si;
-  int64_t lo, hi, r;
-  __device__ __forceinline__ double operator()(int64_t i) const {
-    if (i < hi) {
-      const int k = static_cast<int>(i - lo);
-      DACSR_CHECK(i >= lo);
-      m.check(r, i, si[k]);
-      return product(sv[k], ldg(m.x + m.col(r, si[k])));
-    }
-    return m.prod_global(r, i);
-  }
-};
-
-// One long row, reduced by the whole CTA.
-template <int KIND, class RP, class CI, class VT>
-__device__ void long_row(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int64_t r, int64_t lo,
-                         int64_t hi, const VT* sv, const CI* si, double* scratch) {
-  const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1), len = e - b;
-  StagedGet<KIND, RP, CI, VT> get{m, sv, si, lo, hi, r};
-  if (s.order == DACSR_ORDER_TREE) {
-    double part = 0.0;
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) part = __dadd_rn(part, get(i));
-    const double t = block_sum_tree(part, scratch);
-    if (threadIdx.x == 0) epilogue(m.y, r, t, s.alpha, s.beta);
-    __syncthreads();
-    return;
-  }
-  // exact: warps 1.. produce products of round c+1 while thread 0 folds
-  // round c in the reference order.
-  const int64_t rounds = (len + kLongChunk - 1) / kLongChunk;
-  const int producers = blockDim.x - 32;
-  const int pid = threadIdx.x - 32;
-  auto produce = [&](int64_t c) {
-    double* buf = scratch + (c & 1) * kLongChunk;
-    const int64_t start = b + c * kLongChunk;
-    const int n = static_cast<int>(min64(kLongChunk, e - start));
-    for (int k = pid; k < n; k += producers) buf[k] = get(start + k);
-  };
-  OrderedAcc acc;
-  if (threadIdx.x == 0) acc.init(s.order, len);
-  if (pid >= 0 && rounds > 0) produce(0);
-  __syncthreads();
-  for (int64_t c = 0; c < rounds; ++c) {
-    if (pid >= 0 && c + 1 < rounds) produce(c + 1);
-    if (threadIdx.x == 0) {
-      const double* buf = scratch + (c & 1) * kLongChunk;
-      const int64_t start = c * kLongChunk;
-      const int n = static_cast<int>(min64(kLongChunk, len - start));
-      for (int k = 0; k < n; ++k) acc.add(buf[k]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) epilogue(m.y, r, acc.result(), s.alpha, s.beta);
-  __syncthreads();
-}
-
-// Rows [r0, r1) whose entries are (mostly) staged in smem at [lo, hi).
-// Ends after a __syncthreads: the stage may be overwritten afterwards.
-template <int KIND, class RP, class CI, class VT>
-__device__ void process_rows(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int64_t r0,
-                             int64_t r1, int64_t lo, int64_t hi, const VT* sv, const CI* si,
-                             int64_t* long_rows, int* n_long, double* scratch) {
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1);
-    if (e - b > s.long_len) {
-      long_rows[atomicAdd(n_long, 1)] = r;
-      continue;
-    }
-    StagedGet<KIND, RP, CI, VT> get{m, sv, si, lo, hi, r};
-    epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
-  }
-  __syncthreads();
-  const int nl = *n_long;
-  for (int k = 0; k < nl; ++k) long_row(m, s, long_rows[k], lo, hi, sv, si, scratch);
-}
-
-// ------------------------------------------------- ROWBLOCK (persistent)
-template <int KIND, class RP, class CI, class VT>
-__global__ void __launch_bounds__(kMaxThreads, 2)
-    rowblock_kernel(Mat<KIND, RP, CI, VT> m, Scal s, Chunks p) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ __align__(8) uint64_t full[kMaxStages];
-  __shared__ int64_t long_rows[kMaxLong];
-  __shared__ int n_long;
-
-  const int64_t nb = p.nblocks;
-  if (blockIdx.x >= nb) return;
-  const int64_t mine = (nb - 1 - blockIdx.x) / gridDim.x + 1;
-  const int cap = p.cap, stages = p.stages;
-  const size_t vbytes = static_cast<size_t>(cap) * sizeof(VT);
-  const size_t stage_bytes = static_cast<size_t>(cap) * (sizeof(VT) + sizeof(CI));
-  double* scratch = reinterpret_cast<double*>(dsm + stages * stage_bytes);
-  const int64_t copy_end = p.end & ~int64_t(15);
-
-  auto lo_of = [&](int64_t b) { return p.base + b * cap; };
-  auto hi_of = [&](int64_t b) {
-    const int64_t lo = lo_of(b), hi = min(lo + cap, copy_end);
-    return hi > lo ? hi : lo;
-  };
-  auto issue = [&](int64_t k) {
-    const int64_t b = blockIdx.x + k * gridDim.x;
-    const int st = static_cast<int>(k % stages);
-    const int64_t lo = lo_of(b), hi = hi_of(b);
-    if (hi > lo) {
-      const uint32_t n = static_cast<uint32_t>(hi - lo);
-      unsigned char* dst = dsm + st * stage_bytes;
-      mbar_arrive_expect_tx(&full[st], n * static_cast<uint32_t>(sizeof(VT) + sizeof(CI)));
-      bulk_copy_g2s(dst, m.v + lo, n * sizeof(VT), &full[st]);
-      bulk_copy_g2s(dst + vbytes, m.ci + lo, n * sizeof(CI), &full[st]);
-    }
-  };
-
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < stages; ++st) mbar_init(&full[st], 1);
-    mbar_fence_init();
-    n_long = 0;
-    for (int64_t k = 0; k < min64(stages, mine); ++k) issue(k);
-  }
-  __syncthreads();
-
-  for (int64_t k = 0; k < mine; ++k) {
-    const int64_t b = blockIdx.x + k * gridDim.x;
-    const int st = static_cast<int>(k % stages);
-    const int64_t r0 = ldg(p.block_rows + b), r1 = ldg(p.block_rows + b + 1);
-    const int64_t lo = lo_of(b), hi = hi_of(b);
-    if (hi > lo) mbar_wait(&full[st], static_cast<uint32_t>((k / stages) & 1));
-    const unsigned char* stage = dsm + st * stage_bytes;
-    process_rows(m, s, r0, r1, lo, hi, reinterpret_cast<const VT*>(stage),
-                 reinterpret_cast<const CI*>(stage + vbytes), long_rows, &n_long, scratch);
-    if (threadIdx.x == 0) {
-      n_long = 0;
-      if (k + stages < mine) {
-        fence_proxy_async_smem();
-        issue(k + stages);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------- STAGED (fixed rows per CTA)
-template <int KIND, class RP, class CI, class VT>
-__global__ void __launch_bounds__(256, 4)
-    staged_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t row_start, int64_t row_end, int scap) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int64_t long_rows[256];
-  __shared__ int n_long;
-  __shared__ int64_t s_lo, s_hi;
-
-  const int64_t r0 = row_start + static_cast<int64_t>(blockIdx.x) * blockDim.x;
-  const int64_t r1 = min64(r0 + blockDim.x, row_end);
-  const size_t vbytes = static_cast<size_t>(scap) * sizeof(VT);
-  double* scratch = reinterpret_cast<double*>(dsm + static_cast<size_t>(scap) * (sizeof(VT) + sizeof(CI)));
-  if (threadIdx.x == 0) {
-    const int64_t e0 = ldg(m.rp + r0), e1 = ldg(m.rp + r1);
-    const int64_t lo = e0 & ~int64_t(15);
-    int64_t hi = min64(e1 & ~int64_t(15), lo + scap);
-    if (hi < lo) hi = lo;
-    s_lo = lo;
-    s_hi = hi;
-    n_long = 0;
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-    if (hi > lo) {
-      const uint32_t n = static_cast<uint32_t>(hi - lo);
-      mbar_arrive_expect_tx(&bar, n * static_cast<uint32_t>(sizeof(VT) + sizeof(CI)));
-      bulk_copy_g2s(dsm, m.v + lo, n * sizeof(VT), &bar);
-      bulk_copy_g2s(dsm + vbytes, m.ci + lo, n * sizeof(CI), &bar);
-    }
-  }
-  __syncthreads();
-  const int64_t lo = s_lo, hi = s_hi;
-  if (hi > lo) mbar_wait(&bar, 0);
-  process_rows(m, s, r0, r1, lo, hi, reinterpret_cast<const VT*>(dsm),
-               reinterpret_cast<const CI*>(dsm + vbytes), long_rows, &n_long, scratch);
-}
-
-// ----------------------------------------------------------- SCALAR
-template <int KIND, class RP, class CI, class VT>
-__global__ void __launch_bounds__(256)
-    scalar_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t row_start, int64_t row_end) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t r = row_start + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-       r < row_end; r += stride) {
-    const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1);
-    auto get = [&](int64_t i) { return m.prod_global(r, i); };
-    epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
-  }
-}
-
-// ----------------------------------------------------------- VECTOR<G>
-template <int G, int KIND, class RP, class CI, class VT>
-__global__ void __launch_bounds__(256)
-    vector_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t row_start, int64_t row_end) {
-  constexpr int kGroups = 32 / G;
-  const int lane = threadIdx.x & 31, sub = lane % G, grp = lane / G;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t base = row_start + warp * kGroups; base < row_end; base += nwarps * kGroups) {
-    const int64_t r = base + grp;
-    double acc = 0.0;
-    int64_t b = 0, e = 0;
-    if (r < row_end) {
-      b = ldg(m.rp + r);
-      e = ldg(m.rp + r + 1);
-    }
-    for (int64_t i = b + sub; i < e; i += G) acc = __dadd_rn(acc, m.prod_global(r, i));
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-    if (sub == 0 && r < row_end) epilogue(m.y, r, acc, s.alpha, s.beta);
-  }
-}
-
-// ------------------------------------------------- WSTREAM (warp streams)
-// Each warp owns chunks of 32 consecutive rows (one per lane), chunk c =
-// gw, gw + W, ... (persistent grid).  The chunk's entries [A, A + VCAP)
-// (A = first entry rounded down to 16 bytes of both arrays) are moved into a
-// warp-private shared-memory slot by the TMA bulk-copy engine: lane 0 issues
-// one cp.async.bulk per array, completion is tracked by a per-slot mbarrier
-// (expect_tx).  Two slots per warp: the copy of the warp's next chunk is in
-// flight while the lanes reduce the current one — no registers spent on
-// staging, no CTA-wide barrier, warps pipeline independently.  Rows are
-// reduced one lane per row in the exact reference order; entries past the
-// staged window come from global; rows longer than long_len are reduced by
-// the whole warp after the others.
-// Shared-memory layout of one warp: two slots of `vcap` entries (values,
-// then inner indices, each 16-byte aligned).  vcap is chosen per matrix by
-// the planner (a multiple of 16 covering ~99% of the 32-row chunks).
-template <class RP, class CI, class VT>
-struct WarpChunk {
-  static constexpr int kSlots = 2;
-  // entries per 16-byte vector of the narrower array: window alignment
-  static constexpr int kAlign = 16 / (sizeof(VT) < sizeof(CI) ? sizeof(VT) : sizeof(CI));
-  __host__ __device__ static constexpr int value_bytes(int vcap) {
-    return vcap * static_cast<int>(sizeof(VT));
-  }
-  __host__ __device__ static constexpr int slot_bytes(int vcap) {
-    return value_bytes(vcap) + ((vcap * static_cast<int>(sizeof(CI)) + 15) & ~15);
-  }
-  __host__ __device__ static constexpr int warp_bytes(int vcap) { return kSlots * slot_bytes(vcap); }
-};
-
-// One row reduced by a whole warp.  TREE: lane partial sums + shfl tree.
-// Exact: 128 products per batch go to a warp scratch in shared memory and
-// lane 0 folds them in the reference order, while the next batch's gathers
-// are already in flight.
-template <int KIND, class RP, class CI, class VT>
-__device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s, int64_t r,
-                                           int64_t b, int64_t e, const VT* sv, const CI* si,
-                                           int64_t A, int64_t H, int lane, double* scratch) {
-  auto get = [&](int64_t i) -> double {
-    if (i < H) {
-      const int k = static_cast<int>(i - A);
-      DACSR_CHECK(i >= A);
-      m.check(r, i, si[k]);
-      return product(sv[k], ldg(m.x + m.col(r, si[k])));
-    }
-    return m.prod_global(r, i);
-  };
-  if (s.order == DACSR_ORDER_TREE) {
-    double part = 0.0;
-    for (int64_t i = b + lane; i < e; i += 32) part = __dadd_rn(part, get(i));
-    for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-    if (lane == 0) epilogue(m.y, r, part, s.alpha, s.beta);
-    return;
-  }
-  constexpr int kPer = 4;  // products per lane per batch
-  OrderedAcc acc;
-  acc.init(s.order, e - b);
-  double p[kPer];
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const int64_t i = b + u * 32 + lane;
-    p[u] = i < e ? get(i) : 0.0;
-  }
-  for (int64_t base = b; base < e; base += 32 * kPer) {
-    __syncwarp();
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) scratch[u * 32 + lane] = p[u];
-    __syncwarp();
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {  // next batch in flight during the fold
-      const int64_t i = base + 32 * kPer + u * 32 + lane;
-      p[u] = i < e ? get(i) : 0.0;
-    }
-    if (lane == 0) {
-      const int n = static_cast<int>(min64(32 * kPer, e - base));
-      for (int k = 0; k < n; ++k) acc.add(scratch[k]);
-    }
-  }
-  __syncwarp();
-  if (lane == 0) epilogue(m.y, r, acc.result(), s.alpha, s.beta);
-}
-
-// Chunks the planner listed as not fitting the staging window: one warp per
-// chunk, rows reduced from global in the exact order, long rows by the warp.
-template <int KIND, class RP, class CI, class VT>
-__device__ __noinline__ void complex_chunks(const Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs,
-                                            int64_t re, const int64_t* __restrict__ chunks,
-                                            int64_t n_chunks, int rows_per_chunk, int cta,
-                                            int n_ctas, double* scratch) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = static_cast<int64_t>(n_ctas) * (blockDim.x >> 5);
-  double* wscratch = scratch + (threadIdx.x >> 5) * 128;
-  const int sub = rows_per_chunk / 32;  // 32-row pieces per listed chunk
-  for (int64_t w = static_cast<int64_t>(cta) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       w < n_chunks * sub; w += nw) {
-    const int64_t r = rs + rows_per_chunk * ldg(chunks + w / sub) + 32 * (w % sub) + lane;
-    int64_t b = 0, e = 0;
-    if (r < re) {
-      b = ldg(m.rp + r);
-      e = ldg(m.rp + r + 1);
-    }
-    const bool is_long = (e - b) > s.long_len;
-    if (r < re && !is_long) {
-      auto get = [&](int64_t i) { return m.prod_global(r, i); };
-      epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
-    }
-    unsigned longs = __ballot_sync(0xffffffffu, r < re && is_long);
-    while (longs) {
-      const int src = __ffs(longs) - 1;
-      longs &= longs - 1;
-      const int64_t lb = __shfl_sync(0xffffffffu, b, src), le = __shfl_sync(0xffffffffu, e, src);
-      warp_long_row(m, s, r - lane + src, lb, le, static_cast<const VT*>(nullptr),
-                    static_cast<const CI*>(nullptr), 0, 0, lane, wscratch);
-    }
-  }
-}
-
-// Fully staged row, exact order, from the warp's smem slot.
-// xr = &x[column base of this row]; all gathers of a batch are issued before
-// the first product is folded.
-// Eight gathers x[xr + off[u]] for u < cnt, issued by ONE asm statement so
-// the compiler cannot interleave the fold between them: all eight are in
-// flight before the first product is formed (ILP 8 per lane).
-__device__ __forceinline__ void gather8(const double* xr, const int* off, int cnt, double* v) {
-  const double* p[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) p[u] = xr + off[u];
-  asm volatile(
-      "{\n\t.reg .pred q<8>;\n\t"
-      "setp.gt.s32 q0, %16, 0;\n\tsetp.gt.s32 q1, %16, 1;\n\t"
-      "setp.gt.s32 q2, %16, 2;\n\tsetp.gt.s32 q3, %16, 3;\n\t"
-      "setp.gt.s32 q4, %16, 4;\n\tsetp.gt.s32 q5, %16, 5;\n\t"
-      "setp.gt.s32 q6, %16, 6;\n\tsetp.gt.s32 q7, %16, 7;\n\t"
-      "@q0 ld.global.nc.f64 %0, [%8];\n\t@q1 ld.global.nc.f64 %1, [%9];\n\t"
-      "@q2 ld.global.nc.f64 %2, [%10];\n\t@q3 ld.global.nc.f64 %3, [%11];\n\t"
-      "@q4 ld.global.nc.f64 %4, [%12];\n\t@q5 ld.global.nc.f64 %5, [%13];\n\t"
-      "@q6 ld.global.nc.f64 %6, [%14];\n\t@q7 ld.global.nc.f64 %7, [%15];\n\t}"
-      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]),
-        "=d"(v[7])
-      : "l"(p[0]), "l"(p[1]), "l"(p[2]), "l"(p[3]), "l"(p[4]), "l"(p[5]), "l"(p[6]), "l"(p[7]),
-        "r"(cnt));
-}
-__device__ __forceinline__ void gather8(const float* xr, const int* off, int cnt, float* v) {
-  const float* p[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) p[u] = xr + off[u];
-  asm volatile(
-      "{\n\t.reg .pred q<8>;\n\t"
-      "setp.gt.s32 q0, %16, 0;\n\tsetp.gt.s32 q1, %16, 1;\n\t"
-      "setp.gt.s32 q2, %16, 2;\n\tsetp.gt.s32 q3, %16, 3;\n\t"
-      "setp.gt.s32 q4, %16, 4;\n\tsetp.gt.s32 q5, %16, 5;\n\t"
-      "setp.gt.s32 q6, %16, 6;\n\tsetp.gt.s32 q7, %16, 7;\n\t"
-      "@q0 ld.global.nc.f32 %0, [%8];\n\t@q1 ld.global.nc.f32 %1, [%9];\n\t"
-      "@q2 ld.global.nc.f32 %2, [%10];\n\t@q3 ld.global.nc.f32 %3, [%11];\n\t"
-      "@q4 ld.global.nc.f32 %4, [%12];\n\t@q5 ld.global.nc.f32 %5, [%13];\n\t"
-      "@q6 ld.global.nc.f32 %6, [%14];\n\t@q7 ld.global.nc.f32 %7, [%15];\n\t}"
-      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
-        "=f"(v[7])
-      : "l"(p[0]), "l"(p[1]), "l"(p[2]), "l"(p[3]), "l"(p[4]), "l"(p[5]), "l"(p[6]), "l"(p[7]),
-        "r"(cnt));
-}
-
-template <int ORDER, class CI, class VT>
-__device__ __forceinline__ double staged_dot(const VT* pv, const CI* pi, int n,
-                                             const VT* __restrict__ xr) {
-  if constexpr (ORDER == DACSR_ORDER_NAIVE) {
-    double acc = 0.0;
-    for (int j = 0; j < n; j += 8) {
-      const int cnt = n - j;
-      VT xv[8];
-      if constexpr (sizeof(VT) == 8) {
-        // f64: one asm statement for the 8 gathers (measured: 7 of 8 issued
-        // before the first fold vs 4+4 from the plain loop; C2 33.2 -> 32.4 us)
-        int off[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) off[u] = u < cnt ? static_cast<int>(pi[j + u]) : 0;
-        gather8(xr, off, cnt, xv);
-      } else {
-        // f32: the plain loop measured faster (26.9 vs 29.1 us on C2 f32)
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (u < cnt) xv[u] = ldg(xr + pi[j + u]);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (u < cnt) acc = __dadd_rn(acc, product(pv[j + u], xv[u]));
-    }
-    return acc;
-  } else {
-    auto get = [&](int64_t i) -> double { return product(pv[i], ldg(xr + pi[i])); };
-    return ORDER == DACSR_ORDER_MACC3 ? sum_macc3(0, n, get) : sum_strip4(0, n, get);
-  }
-}
-
-__device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// Chunks of 32 rows whose entries [first, last) fit the staging window
-// [A, A + VCAP) with A = first rounded down to 16 bytes ("simple").  The
-// planner lists the others; the hot kernel skips them.
-template <class IT>
-__device__ __forceinline__ bool chunk_fits(IT first, IT last, int vcap, int align, IT last_aligned) {
-  const IT A = first & ~static_cast<IT>(align - 1);
-  IT H = A + vcap;
-  if (H > last_aligned) H = last_aligned;
-  return last <= H;
-}
-
-// 64 registers (4 CTAs/SM): measured faster than 48 registers at 5 CTAs/SM
-// (C2: 33.5 vs 39.0 us) — the gather batch needs the registers for ILP.
-#ifndef DACSR_WSTREAM_MINB
-#define DACSR_WSTREAM_MINB 4
-#endif
-template <int KIND, class RP, class CI, class VT, int ORDER, int RPL>
-__global__ void __launch_bounds__(256, DACSR_WSTREAM_MINB)
-    wstream_kernel(Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs, int64_t re, int64_t nnz,
-                   const int64_t* complex_list, int64_t n_complex, int side_ctas, int vcap) {
-  using WC = WarpChunk<RP, CI, VT>;
-  constexpr int kRows = 32 * RPL;         // rows per chunk (RPL per lane)
-  constexpr int kRpSlot = kRows + 8;      // rowptr values per slot (kRows + 1 used)
-  const int kSlot = WC::slot_bytes(vcap), kVB = WC::value_bytes(vcap);
-  extern __shared__ __align__(128) unsigned char dsm[];
-  // Programmatic dependent launch: the next launch in the stream may start
-  // its prologue (matrix-only reads) while this grid drains; x and y are
-  // touched only after griddepcontrol.wait (the previous grid complete).
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // the first side_ctas CTAs take the planner's complex chunks, so they are
-  // resident from the start and overlap the streaming CTAs
-  if (static_cast<int>(blockIdx.x) < side_ctas) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    complex_chunks(m, s, rs, re, complex_list, n_complex, kRows, blockIdx.x, side_ctas,
-                   reinterpret_cast<double*>(dsm));
-    return;
-  }
-  const int cta = blockIdx.x - side_ctas, n_cta = gridDim.x - side_ctas;
-  using IT = RP;  // entry positions fit the rowptr type
-  __shared__ __align__(8) uint64_t bars[8][WC::kSlots];
-  __shared__ RP rps[8][3][kRpSlot];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  unsigned char* wbase = dsm + wib * WC::warp_bytes(vcap);
-  uint64_t* bar = bars[wib];
-  RP (*rp_slot)[kRpSlot] = rps[wib];
-  const int W = n_cta * (blockDim.x >> 5);
-  const int gw = cta * (blockDim.x >> 5) + wib;
-  const int nchunks = static_cast<int>((re - rs + kRows - 1) / kRows);
-  if (gw >= nchunks) return;
-  const IT last_aligned = static_cast<IT>(nnz & ~int64_t(WC::kAlign - 1));
-
-  if (lane == 0) {
-    for (int k = 0; k < WC::kSlots; ++k) mbar_init(&bar[k], 1);
-    mbar_fence_init();
-  }
-  // rowptr slice of chunk c: lane l copies rowptr[rs + kRows*c + 32q + l + 1]
-  // (clamped) for q < RPL, lane 0 also rowptr[rs + kRows*c]
-  auto fetch_rp = [&](int c, int slot) {
-    if (c < nchunks) {
-      const int64_t row0 = rs + kRows * static_cast<int64_t>(c);
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const RP* src = m.rp + min64(row0 + 32 * q + lane + 1, re);
-        if constexpr (sizeof(RP) == 8) cp_async_8(&rp_slot[slot][32 * q + lane + 1], src);
-        else cp_async_4(&rp_slot[slot][32 * q + lane + 1], src);
-      }
-      if (lane == 0) {
-        if constexpr (sizeof(RP) == 8) cp_async_8(&rp_slot[slot][0], m.rp + row0);
-        else cp_async_4(&rp_slot[slot][0], m.rp + row0);
-      }
-    }
-    cp_async_commit();
-  };
-  // lane 0: the chunk's entries via the TMA bulk-copy engine
-  auto issue = [&](int slot, IT first) {
-    const IT A = first & ~static_cast<IT>(WC::kAlign - 1);
-    IT H = A + vcap;
-    if (H > last_aligned) H = last_aligned;
-    if (H > A) {
-      const uint32_t n = static_cast<uint32_t>(H - A);
-      unsigned char* dst = wbase + slot * kSlot;
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&bar[slot], n * static_cast<uint32_t>(sizeof(VT) + sizeof(CI)));
-      bulk_copy_g2s(dst, m.v + A, n * sizeof(VT), &bar[slot]);
-      bulk_copy_g2s(dst + kVB, m.ci + A, ((n * sizeof(CI)) + 15) & ~15u, &bar[slot]);
-    }
-  };
-  auto fits = [&](int slot) {
-    return chunk_fits<IT>(rp_slot[slot][0], rp_slot[slot][kRows], vcap, WC::kAlign, last_aligned);
-  };
-  // a chunk's entries are copied (and waited for) iff it fits and is not
-  // empty; both sides evaluate this same predicate
-  auto staged = [&](int slot) {
-    const IT A = rp_slot[slot][0] & ~static_cast<IT>(WC::kAlign - 1);
-    return fits(slot) && rp_slot[slot][kRows] > A;
-  };
-
-  fetch_rp(gw, 0);
-  fetch_rp(gw + W, 1);
-  cp_async_wait<1>();
-  __syncwarp();
-  // per chunk, `fits` and `staged` are evaluated once (when its rowptr
-  // slice lands) and carried to the iteration that consumes the chunk
-  bool fits_cur = fits(0), staged_cur = staged(0);
-  if (lane == 0 && staged_cur) issue(0, rp_slot[0][0]);
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y from here on
-  uint32_t phase = 0;
-  int rslot = 0;
-  int k = 0;
-  const VT* __restrict__ xbase = m.x + m.xoff;
-  for (int c = gw; c < nchunks; c += W, ++k) {
-    const int dslot = k & 1;
-    const int rnext = rslot == 2 ? 0 : rslot + 1;
-    const int rnn = rnext == 2 ? 0 : rnext + 1;
-    cp_async_wait<0>();  // rowptr of chunk c + W (issued last iteration)
-    __syncwarp();
-    const bool has_next = c + W < nchunks;
-    const bool fits_next = has_next && fits(rnext);
-    const bool staged_next = fits_next && staged(rnext);
-    if (lane == 0 && staged_next) issue(dslot ^ 1, rp_slot[rnext][0]);
-    fetch_rp(c + 2 * W, rnn);
-    if (fits_cur) {  // warp-uniform: complex chunks belong to the side CTAs
-      if (staged_cur) {
-        mbar_wait(&bar[dslot], (phase >> dslot) & 1u);
-        phase ^= 1u << dslot;
-      }
-      const IT A = rp_slot[rslot][0] & ~static_cast<IT>(WC::kAlign - 1);
-      const VT* sv = reinterpret_cast<const VT*>(wbase + dslot * kSlot);
-      const CI* si = reinterpret_cast<const CI*>(wbase + dslot * kSlot + kVB);
-      const int64_t row0 = rs + kRows * static_cast<int64_t>(c);
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const int rl = 32 * q + lane;
-        if (row0 + rl < re) {
-          const int64_t r = row0 + rl;
-          const IT b = rp_slot[rslot][rl], e = rp_slot[rslot][rl + 1];
-          const int kk = static_cast<int>(b - A);
-          DACSR_CHECK(kk >= 0 && kk + (e - b) <= vcap && e >= b);
-#ifdef DACSR_CHECKED
-          for (int j = 0; j < static_cast<int>(e - b); ++j)
-            m.check(r, b + j, reinterpret_cast<const CI*>(wbase + dslot * kSlot + kVB)[kk + j]);
-#endif
-          const VT* xr = KIND == DACSR_KIND_DA ? xbase + r : xbase;
-          epilogue(m.y, r, staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b), xr),
-                   s.alpha, s.beta);
-        }
-      }
-    }
-    __syncwarp();
-    fits_cur = fits_next;
-    staged_cur = staged_next;
-    rslot = rnext;
-  }
-  cp_async_wait<0>();
-}
-
-// planner: list the 32-row chunks that do not fit a VCAP window
-template <class RP>
-__global__ void classify_chunks_kernel(const RP* __restrict__ rp, int64_t rs, int64_t re,
-                                       int rows, int vcap, int align, int64_t last_aligned,
-                                       int64_t* out, unsigned long long* count) {
-  const int64_t nchunks = (re - rs + rows - 1) / rows;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < nchunks;
-       c += stride) {
-    const int64_t first = static_cast<int64_t>(rp[rs + rows * c]);
-    const int64_t last = static_cast<int64_t>(rp[min64(rs + rows * c + rows, re)]);
-    if (!chunk_fits<int64_t>(first, last, vcap, align, last_aligned)) {
-      const unsigned long long slot = atomicAdd(count, 1ull);
-      out[slot] = c;
-    }
-  }
-}
-
-// ============================================================ host side
-namespace {
-
-int sm_count() {
-  static int cached = -1;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  if (cached < 0) {
-    int v = 0;
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
-      v = 148;
-    cached = v;
-  }
-  return cached;
-}
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-// Per-kernel launch configuration, computed once per (kernel, smem bytes):
-// the max-dynamic-smem attribute and the occupancy query cost microseconds
-// of host time, which would otherwise sit between back-to-back launches.
-// The attribute is raised once per kernel to the device's opt-in maximum
-// (it is a cap, not a reservation), so cached entries stay launchable.
-struct LaunchCache {
-  std::mutex mu;
-  const void* fn[96] = {};
-  size_t smem[96] = {};
-  int per_sm[96] = {};
-  int n = 0;
-  const void* raised[96] = {};
-  int n_raised = 0;
-};
-
-template <class K>
-int cached_per_sm(K kern, int threads, size_t smem) {
-  static LaunchCache cache;
-  const void* key = reinterpret_cast<const void*>(kern);
-  std::lock_guard<std::mutex> lock(cache.mu);
-  for (int i = 0; i < cache.n; ++i)
-    if (cache.fn[i] == key && cache.smem[i] == smem) return cache.per_sm[i];
-  bool raised = false;
-  for (int i = 0; i < cache.n_raised; ++i) raised |= cache.raised[i] == key;
-  if (!raised) {
-    int dev = 0, optin = 227 * 1024;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return -1;
-    const int dyn_max = optin - static_cast<int>(fa.sharedSizeBytes);
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) !=
-        cudaSuccess)
-      return -1;
-    if (cache.n_raised < 96) cache.raised[cache.n_raised++] = key;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess)
-    return -1;
-  per_sm = std::max(1, per_sm);
-  if (cache.n < 96) {
-    cache.fn[cache.n] = key;
-    cache.smem[cache.n] = smem;
-    cache.per_sm[cache.n] = per_sm;
-    ++cache.n;
-  }
-  return per_sm;
-}
-
-struct Req {
-  const dacsr_plan_t* plan;
-  int variant, order;
-  const void* x;
-  int64_t xoff;
-  void* y;
-  double alpha, beta;
-  int64_t rs, re;
-  cudaStream_t stream;
-};
-
-template <class VT, class CI>
-int rowblock_stages(int cap) {
-  const size_t stage = static_cast<size_t>(cap) * (sizeof(VT) + sizeof(CI));
-  const size_t budget = 100 * 1024;
-  int st = static_cast<int>(budget / stage);
-  return std::max(2, std::min(kMaxStages, st));
-}
-
-template <int KIND, class RP, class CI, class VT>
-int launch(const dacsr_matrix_t* a, const Req& q) {
-  Mat<KIND, RP, CI, VT> m{static_cast<const RP*>(a->rowptr), static_cast<const CI*>(a->colids),
-                          static_cast<const VT*>(a->values), static_cast<const VT*>(q.x),
-                          static_cast<VT*>(q.y), q.xoff, a->nrows,
-                          a->ncols > 0 ? a->ncols : INT64_MAX,
-                          a->nnz > 0 ? a->nnz : INT64_MAX};
-  const int64_t rows = q.re - q.rs;
-  if (rows <= 0) return DACSR_OK;
-  const int order = q.order;
-  const bool exact = order != DACSR_ORDER_TREE;
-  Scal s{q.alpha, q.beta, order, 0};
-  const int sms = sm_count();
-  const bool can_bulk = aligned16(a->values) && aligned16(a->colids);
-
-  switch (q.variant) {
-    case DACSR_VARIANT_ROWBLOCK: {
-      const dacsr_plan_t* p = q.plan;
-      if (!p || p->row_start != q.rs || p->row_end != q.re || !p->block_rows) return DACSR_ERR_PLAN;
-      if (p->cap <= 0 || (p->cap & 15) || !can_bulk) return DACSR_ERR_PLAN;
-      // at most cap/long_len + 1 long rows can start inside one chunk
-      s.long_len = std::max<int64_t>(p->long_len, p->cap / (kMaxLong - 2));
-      const int stages = rowblock_stages<VT, CI>(p->cap);
-      const size_t smem = static_cast<size_t>(stages) * p->cap * (sizeof(VT) + sizeof(CI)) + kScratchBytes;
-      auto kern = rowblock_kernel<KIND, RP, CI, VT>;
-      const int threads = kMaxThreads;
-      const int per_sm = cached_per_sm(kern, threads, smem);
-      if (per_sm < 0) return check_launch("rowblock launch config");
-      const int64_t grid = std::min<int64_t>(p->nblocks, static_cast<int64_t>(sms) * per_sm);
-      Chunks c{p->block_rows, p->entry_base, p->entry_end, p->nblocks, p->cap, stages};
-      kern<<<static_cast<unsigned>(grid), threads, smem, q.stream>>>(m, s, c);
-      return check_launch("rowblock_kernel");
-    }
-    case DACSR_VARIANT_STAGED: {
-      const int threads = 256;
-      // capacity: 2x the mean entries of a 256-row block, at most 64 KiB
-      // (the reference-named entry points pass nnz = 0: assume 16 per row)
-      const double mean = a->nnz > 0 && a->nrows ? static_cast<double>(a->nnz) / a->nrows : 16.0;
-      int scap = static_cast<int>(std::min(65536.0 / (sizeof(VT) + sizeof(CI)),
-                                           std::max(512.0, 2.0 * mean * threads)));
-      scap &= ~15;
-      if (!can_bulk) scap = 0;
-      s.long_len = std::max<int64_t>(256, static_cast<int64_t>(8 * mean));
-      const size_t smem = static_cast<size_t>(scap) * (sizeof(VT) + sizeof(CI)) + kScratchBytes;
-      auto kern = staged_kernel<KIND, RP, CI, VT>;
-      if (cached_per_sm(kern, threads, smem) < 0) return check_launch("staged launch config");
-      const int64_t grid = (rows + threads - 1) / threads;
-      kern<<<static_cast<unsigned>(grid), threads, smem, q.stream>>>(m, s, q.rs, q.re, scap);
-      return check_launch("staged_kernel");
-    }
-    case DACSR_VARIANT_SCALAR: {
-      const int threads = 256;
-      const int64_t grid = std::min<int64_t>((rows + threads - 1) / threads, sms * 16);
-      scalar_kernel<KIND, RP, CI, VT><<<static_cast<unsigned>(grid), threads, 0, q.stream>>>(
-          m, s, q.rs, q.re);
-      return check_launch("scalar_kernel");
-    }
-    case DACSR_VARIANT_VECTOR2:
-    case DACSR_VARIANT_VECTOR4:
-    case DACSR_VARIANT_VECTOR8:
-    case DACSR_VARIANT_VECTOR16:
-    case DACSR_VARIANT_WARP: {
-      (void)exact;  // vector variants always combine lanes with a tree
-      const int threads = 256;
-      const int g = 2 << (q.variant - DACSR_VARIANT_VECTOR2);
-      const int64_t rows_per_cta = threads / g;
-      const int64_t grid = std::min<int64_t>((rows + rows_per_cta - 1) / rows_per_cta, sms * 16);
-      const unsigned gr = static_cast<unsigned>(std::max<int64_t>(grid, 1));
-      switch (g) {
-        case 2: vector_kernel<2, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
-        case 4: vector_kernel<4, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
-        case 8: vector_kernel<8, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
-        case 16: vector_kernel<16, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
-        default: vector_kernel<32, KIND, RP, CI, VT><<<gr, threads, 0, q.stream>>>(m, s, q.rs, q.re); break;
-      }
-      return check_launch("vector_kernel");
-    }
-    case DACSR_VARIANT_WSTREAM: {
-      const dacsr_plan_t* p = q.plan;
-      if (!p || p->chunk_vcap <= 0 || (p->chunk_rows != 32 && p->chunk_rows != 64) ||
-          p->row_start != q.rs || p->row_end != q.re ||
-          (p->n_complex > 0 && !p->complex_chunks) || !can_bulk)
-        return DACSR_ERR_PLAN;
-      if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
-        // warp streams specialise the naive order; the others run row blocks
-        Req r2 = q;
-        r2.variant = p->block_rows ? DACSR_VARIANT_ROWBLOCK : DACSR_VARIANT_STAGED;
-        return launch<KIND, RP, CI, VT>(a, r2);
-      }
-      const int vcap = p->chunk_vcap;
-      // side CTAs need 128 doubles of scratch per warp
-      const size_t per_warp = std::max<size_t>(WarpChunk<RP, CI, VT>::warp_bytes(vcap), 128 * 8);
-      // up to 8 warps per CTA within ~200 KiB of shared memory
-      const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp)));
-      const int threads = 32 * warps;
-      s.long_len = std::max<int64_t>(p->long_len, 32);
-      auto kern = p->chunk_rows == 64 ? wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE, 2>
-                                      : wstream_kernel<KIND, RP, CI, VT, DACSR_ORDER_NAIVE, 1>;
-      const size_t smem = per_warp * warps;
-      int per_sm = cached_per_sm(kern, threads, smem);
-      if (per_sm < 0) return check_launch("wstream launch config");
-      if (p->ctas_per_sm > 0) per_sm = std::min(per_sm, static_cast<int>(p->ctas_per_sm));
-      const int64_t chunks = (rows + p->chunk_rows - 1) / p->chunk_rows;
-      // all CTAs co-resident; the complex chunks get at most 1/8 of the
-      // slots (they loop), the streaming grid the rest
-      const int64_t slots = static_cast<int64_t>(sms) * per_sm;
-      const int side = p->n_complex > 0
-                           ? static_cast<int>(std::min<int64_t>((p->n_complex + warps - 1) / warps,
-                                                                std::max<int64_t>(1, slots / 8)))
-                           : 0;
-      const int64_t grid = std::min<int64_t>((chunks + warps - 1) / warps, std::max<int64_t>(slots - side, slots / 2));
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(grid, 1) + side));
-      cfg.blockDim = dim3(threads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = q.stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      const int64_t nnz = a->nnz;
-      const int64_t* cl = p->complex_chunks;
-      const int64_t ncx = p->n_complex;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, q.rs, q.re, nnz, cl, ncx, side, vcap);
-      if (e != cudaSuccess) {
-        set_last_error("wstream_kernel launch", e);
-        return DACSR_ERR_CUDA;
-      }
-      return check_launch("wstream_kernel");
-    }
-    default:
-      return DACSR_ERR_VARIANT;
-  }
-}
-
-template <int KIND, class RP, class CI>
-int by_values(const dacsr_matrix_t* a, const Req& q) {
-  if (a->values_dtype == DACSR_F64) return launch<KIND, RP, CI, double>(a, q);
-  if (a->values_dtype == DACSR_F32) return launch<KIND, RP, CI, float>(a, q);
-  return DACSR_ERR_DTYPE;
-}
-
-template <int KIND, class RP>
-int by_colids(const dacsr_matrix_t* a, const Req& q) {
-  if constexpr (KIND == DACSR_KIND_DA) {
-    switch (a->colids_dtype) {
-      case DACSR_I8: return by_values<KIND, RP, int8_t>(a, q);
-      case DACSR_I16: return by_values<KIND, RP, int16_t>(a, q);
-      case DACSR_I32: return by_values<KIND, RP, int32_t>(a, q);
-      default: return DACSR_ERR_DTYPE;
-    }
-  } else {
-    switch (a->colids_dtype) {
-      case DACSR_I32: return by_values<KIND, RP, int32_t>(a, q);
-      case DACSR_I64: return by_values<KIND, RP, int64_t>(a, q);
-      default: return DACSR_ERR_DTYPE;
-    }
-  }
-}
-
-template <int KIND>
-int by_rowptr(const dacsr_matrix_t* a, const Req& q) {
-  if (a->rowptr_dtype == DACSR_I32) return by_colids<KIND, int32_t>(a, q);
-  if (a->rowptr_dtype == DACSR_I64) return by_colids<KIND, int64_t>(a, q);
-  return DACSR_ERR_DTYPE;
-}
-
-}  // namespace
 }  // namespace dacsr
 
 using namespace dacsr;
@@ -1001,8 +73,8 @@ int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t rs, int64_t re, int32_t c
   if (!a || !inout || !chunks_dev || !count_scratch_dev || rs < 0 || re < rs || re > a->nrows ||
       vcap < 64 || vcap > 16384 || (vcap & 15) || (chunk_rows != 32 && chunk_rows != 64))
     return DACSR_ERR_ARG;
-  static const int kBytes[6] = {1, 2, 4, 8, 4, 8};
-  if (a->values_dtype < 0 || a->values_dtype > 5 || a->colids_dtype < 0 || a->colids_dtype > 5)
+  static const int kBytes[8] = {1, 2, 4, 8, 4, 8, 2, 2};
+  if (a->values_dtype < 0 || a->values_dtype > 7 || a->colids_dtype < 0 || a->colids_dtype > 5)
     return DACSR_ERR_DTYPE;
   const int narrow = std::min(kBytes[a->values_dtype], kBytes[a->colids_dtype]);
   const int align = 16 / narrow;
@@ -1054,9 +126,13 @@ int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t varian
   if (variant == DACSR_VARIANT_AUTO) variant = plan ? DACSR_VARIANT_ROWBLOCK : DACSR_VARIANT_STAGED;
   Req q{plan, variant, order, x, x_offset, y, alpha, beta, row_start, row_end,
         static_cast<cudaStream_t>(stream)};
-  if (a->kind == DACSR_KIND_DA) return by_rowptr<DACSR_KIND_DA>(a, q);
-  if (a->kind == DACSR_KIND_CSR) return by_rowptr<DACSR_KIND_CSR>(a, q);
-  return DACSR_ERR_DTYPE;
+  switch (a->values_dtype) {
+    case DACSR_F64: return launch_values_f64(a, q);
+    case DACSR_F32: return launch_values_f32(a, q);
+    case DACSR_F16: return launch_values_f16(a, q);
+    case DACSR_BF16: return launch_values_bf16(a, q);
+    default: return DACSR_ERR_DTYPE;
+  }
 }
 
 // Host-buffer SpMV with the copies overlapped (see hostpath.py): rows are
@@ -1071,8 +147,8 @@ int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans,
   if (!a || !plans || npieces <= 0 || npieces > 64 || !x_host || !y_host || !x_dev || !y_dev ||
       w < 0)
     return DACSR_ERR_ARG;
-  static const int kBytes[6] = {1, 2, 4, 8, 4, 8};
-  if (a->values_dtype != DACSR_F32 && a->values_dtype != DACSR_F64) return DACSR_ERR_DTYPE;
+  static const int kBytes[8] = {1, 2, 4, 8, 4, 8, 2, 2};
+  if (a->values_dtype < DACSR_F32 || a->values_dtype > DACSR_BF16) return DACSR_ERR_DTYPE;
   const size_t vb = kBytes[a->values_dtype];
   auto h2d = static_cast<cudaStream_t>(s_h2d), comp = static_cast<cudaStream_t>(s_comp),
        d2h = static_cast<cudaStream_t>(s_d2h);

@@ -9,7 +9,9 @@ statistics from ``dacsr_analyze`` and the nnz-balanced ROWBLOCK plan
   widths (int8/int16, reference test_spmv.py:238-247) widen to int32.
 * inner   DA: int8/int16/int32 offsets kept as given (int16 is the paper's
   case, 2 bytes/entry); CSR: int32 (int64 only when ncols > 2^31).
-* values  float32/float64 as given.
+* values  float32/float64 as given; ``astype`` makes float16/bfloat16
+  copies (the width-lattice extension of model.py:21-74: 2-byte values,
+  exact f32 products, f64 accumulation, one rounding on the store).
 All arrays are unpadded and 16-byte aligned (torch allocations are 512-byte
 aligned), which the TMA bulk copies require; kernels never read past nnz.
 
@@ -262,6 +264,19 @@ class DeviceMatrix:
     @property
     def dtype(self):
         return self.values.dtype
+
+    def astype(self, dtype, plan=True):
+        """The same operator with values converted on the device (torch's
+        rounding) to ``dtype`` (float16/bfloat16/float32/float64); rowptr and
+        offsets are shared.  x and y must then carry the same dtype."""
+        dtype = getattr(torch, dtype) if isinstance(dtype, str) else dtype
+        if dtype not in (torch.float16, torch.bfloat16, torch.float32, torch.float64):
+            raise ValueError(f"unsupported value dtype {dtype}")
+        if dtype == self.values.dtype:
+            return self
+        return DeviceMatrix(self.kind, self.nrows, self.ncols, self.rowptr, self.colids,
+                            self.values.to(dtype), plan=plan, row_start=self.row_start,
+                            row_end=self.row_end)
 
     def storage_bytes(self):
         return sum(t.numel() * t.element_size() for t in (self.rowptr, self.colids, self.values))

@@ -135,6 +135,10 @@ def kernel_for(dm, kname, order):
     return kname
 
 
+_SCALARS = ("float32", "float64")
+_SCALARS_16 = ("float16", "bfloat16")  # DeviceMatrix.astype extension only
+
+
 def _is_host(v):
     return isinstance(v, np.ndarray)
 
@@ -178,7 +182,7 @@ def spmv(a, x, y=None, alpha=1.0, beta=0.0, variant="naive", backend=None, *, st
             raise TypeError("y must be a numpy array or torch tensor (it is updated in place)")
         if tuple(y.shape) != (nrows,):
             raise DimensionMismatch(f"y has shape {tuple(y.shape)}, expected ({nrows},)")
-    if vdtype not in ("float32", "float64"):
+    if vdtype not in _SCALARS and not (isinstance(a, DeviceMatrix) and vdtype in _SCALARS_16):
         raise UnsupportedScalarWidth(f"unsupported scalar dtype {vdtype}")
     ydtype = vdtype if fresh else _dtype_name(y)
     if _dtype_name(x) != vdtype or ydtype != vdtype:
