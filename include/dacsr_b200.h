@@ -66,9 +66,14 @@ enum {
   DACSR_VARIANT_VECTOR16 = 6,
   DACSR_VARIANT_WARP = 7,
   DACSR_VARIANT_STAGED = 8,   /* fixed rows per CTA, TMA-bulk staged (no plan)   */
-  DACSR_VARIANT_WSTREAM = 9   /* warp streams: 32-row chunks per warp, TMA bulk  */
+  DACSR_VARIANT_WSTREAM = 9,  /* warp streams: 32-row chunks per warp, TMA bulk  */
                               /* double-buffered per warp, exact naive order;    */
                               /* staging window from the plan (chunk_vcap)       */
+  DACSR_VARIANT_SLICED = 10,  /* sliced layout (plan->slices): lane per row,     */
+                              /* coalesced column-major entries straight from    */
+                              /* HBM, exact naive order; spill rows by side warps*/
+  DACSR_VARIANT_SLICED_TMA = 11 /* sliced layout, each warp's next two slices    */
+                              /* staged in smem by TMA bulk copies              */
 };
 
 /* A matrix in CSR (absolute colids) or DA-CSR (colids = col - row) layout.
@@ -85,6 +90,47 @@ typedef struct {
   const void* colids;
   const void* values;
 } dacsr_matrix_t;
+
+/* Sliced device layout of rows [row_start, row_end) — a derived copy of the
+ * entries in HBM (the CSR/DA-CSR arrays stay the reference layout).
+ *
+ * Main slices: slice s holds rows row_start + 32s + lane (lane 0..31);
+ * entry j of that row sits at slot slice_ptr[s] + 32*j + lane of `inner` /
+ * `values`, so the 32 lanes of a warp read entry j of their rows as one
+ * contiguous 32-element run.  Width W_s = (slice_ptr[s+1] - slice_ptr[s]) /
+ * 32 = the longest row of the slice with at most max_len entries; shorter
+ * rows are zero-padded (never read), longer rows are not in main slices.
+ *
+ * Medium rows (max_len < len <= medium_len) are listed ascending in
+ * medium_rows and packed 32 per "medium slice" the same way (lane l of
+ * medium slice m = row medium_rows[32m + l]; slots in m_slice_ptr /
+ * m_inner / m_values).  Long rows (len > medium_len) are listed ascending
+ * in long_rows and reduced by a whole warp from the CSR arrays.
+ *
+ * row_len[r - row_start] = entries of row r, or 255 if the row has more
+ * than 254.  max_len <= medium_len <= 254.  All buffers are device memory
+ * owned by the caller; entries are bit-for-bit copies, in row order. */
+typedef struct {
+  int64_t row_start;
+  int64_t row_end;
+  int64_t nslices;          /* ceil((row_end - row_start) / 32)              */
+  int64_t total;            /* main slots = slice_ptr[nslices]               */
+  int32_t max_len;          /* main-slice rows: len <= max_len               */
+  int32_t medium_len;       /* medium rows: max_len < len <= medium_len      */
+  const int64_t* slice_ptr; /* nslices + 1                                   */
+  const uint8_t* row_len;   /* row_end - row_start                           */
+  const void* inner;        /* total, the matrix's colids dtype              */
+  const void* values;       /* total, the matrix's values dtype              */
+  int64_t n_medium;
+  int64_t m_nslices;        /* ceil(n_medium / 32)                           */
+  int64_t m_total;          /* m_slice_ptr[m_nslices]                        */
+  const int64_t* medium_rows; /* n_medium, ascending                         */
+  const int64_t* m_slice_ptr; /* m_nslices + 1                               */
+  const void* m_inner;
+  const void* m_values;
+  int64_t n_long;
+  const int64_t* long_rows; /* n_long, ascending                             */
+} dacsr_slices_t;
 
 /* Row-length statistics of rows [row_start, row_end). */
 typedef struct {
@@ -116,8 +162,10 @@ typedef struct {
   int32_t chunk_rows;  /* rows per warp chunk: 32 (1 per lane) or 64 (2)     */
   int64_t n_complex;
   const int64_t* complex_chunks; /* device, n_complex chunk indices          */
-  int32_t ctas_per_sm; /* WSTREAM resident CTAs per SM (0 = occupancy max)    */
+  int32_t ctas_per_sm; /* WSTREAM/SLICED resident CTAs per SM (0 = max)      */
   int32_t reserved;
+  /* SLICED: the layout (its row range must contain the launch's rows).     */
+  const dacsr_slices_t* slices;
 } dacsr_plan_t;
 
 const char* dacsr_version(void);
@@ -150,6 +198,26 @@ int dacsr_plan_build(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end
 int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end,
                       int32_t chunk_rows, int32_t vcap, int64_t* chunks_dev,
                       void* count_scratch_dev, dacsr_plan_t* inout, void* stream);
+
+/* Sliced layout builder (warp per slice; scans with dacsr_counts_to_rowptr
+ * into int64 between the passes; the caller sizes the buffers from the
+ * scanned totals).
+ * 1. dacsr_slices_count: row_len_dev[r - row_start]; per main slice
+ *    slot_counts[s] = 32 * W_s, medium_counts[s], long_counts[s] (int32).
+ * 2. dacsr_slices_fill: s->inner / s->values (padding zeroed), the medium
+ *    and long row lists (medium_ptr / long_ptr: the scanned counts).
+ * 3. dacsr_slices_medium_count: m_slot_counts[m] = 32 * width of medium
+ *    slice m (needs s->medium_rows, s->row_len).
+ * 4. dacsr_slices_medium_fill: s->m_inner / s->m_values.
+ * 1 <= max_len <= medium_len <= 254. */
+int dacsr_slices_count(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end,
+                       int32_t max_len, int32_t medium_len, uint8_t* row_len_dev,
+                       int32_t* slot_counts_dev, int32_t* medium_counts_dev,
+                       int32_t* long_counts_dev, void* stream);
+int dacsr_slices_fill(const dacsr_matrix_t* a, const dacsr_slices_t* s,
+                      const int64_t* medium_ptr_dev, const int64_t* long_ptr_dev, void* stream);
+int dacsr_slices_medium_count(const dacsr_slices_t* s, int32_t* m_slot_counts_dev, void* stream);
+int dacsr_slices_medium_fill(const dacsr_matrix_t* a, const dacsr_slices_t* s, void* stream);
 
 /* Variant the library would run for DACSR_VARIANT_AUTO. */
 int32_t dacsr_select_variant(const dacsr_stats_t* stats, int32_t order);

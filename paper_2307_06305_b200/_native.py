@@ -26,7 +26,7 @@ KIND_CSR, KIND_DA = 0, 1
 ORDER_NAIVE, ORDER_MACC3, ORDER_STRIP4, ORDER_TREE = range(4)
 VARIANT_CODES = {
     "auto": 0, "rowblock": 1, "scalar": 2, "vector2": 3, "vector4": 4, "vector8": 5,
-    "vector16": 6, "warp": 7, "staged": 8, "wstream": 9,
+    "vector16": 6, "warp": 7, "staged": 8, "wstream": 9, "sliced": 10, "sliced_tma": 11,
 }
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported dtype", 3: "unknown variant/order",
           4: "CUDA error", 5: "plan mismatch"}
@@ -67,7 +67,22 @@ class Plan(ctypes.Structure):
                 ("long_len", ctypes.c_int32), ("block_rows", ctypes.c_void_p),
                 ("chunk_vcap", ctypes.c_int32), ("chunk_rows", ctypes.c_int32),
                 ("n_complex", ctypes.c_int64), ("complex_chunks", ctypes.c_void_p),
-                ("ctas_per_sm", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("ctas_per_sm", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("slices", ctypes.c_void_p)]
+
+
+class Slices(ctypes.Structure):
+    """dacsr_slices_t: the sliced device layout (32-row slices)."""
+    _fields_ = [("row_start", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("nslices", ctypes.c_int64), ("total", ctypes.c_int64),
+                ("max_len", ctypes.c_int32), ("medium_len", ctypes.c_int32),
+                ("slice_ptr", ctypes.c_void_p), ("row_len", ctypes.c_void_p),
+                ("inner", ctypes.c_void_p), ("values", ctypes.c_void_p),
+                ("n_medium", ctypes.c_int64), ("m_nslices", ctypes.c_int64),
+                ("m_total", ctypes.c_int64), ("medium_rows", ctypes.c_void_p),
+                ("m_slice_ptr", ctypes.c_void_p), ("m_inner", ctypes.c_void_p),
+                ("m_values", ctypes.c_void_p), ("n_long", ctypes.c_int64),
+                ("long_rows", ctypes.c_void_p)]
 
 
 def typed_kernel_names():
@@ -89,6 +104,11 @@ _SIGNATURES = {
     "dacsr_plan_build": ([_P(Matrix), _i64, _i64, _i64, _i64, _i32, _i32, _vp, _P(Plan), _vp],
                          ctypes.c_int),
     "dacsr_select_variant": ([_P(Stats), _i32], _i32),
+    "dacsr_slices_count": ([_P(Matrix), _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
+                           ctypes.c_int),
+    "dacsr_slices_fill": ([_P(Matrix), _P(Slices), _vp, _vp, _vp], ctypes.c_int),
+    "dacsr_slices_medium_count": ([_P(Slices), _vp, _vp], ctypes.c_int),
+    "dacsr_slices_medium_fill": ([_P(Matrix), _P(Slices), _vp], ctypes.c_int),
     "dacsr_plan_chunks": ([_P(Matrix), _i64, _i64, _i32, _i32, _vp, _vp, _P(Plan), _vp],
                           ctypes.c_int),
     "dacsr_spmv": ([_P(Matrix), _P(Plan), _i32, _i32, _vp, _i64, _vp, _d, _d, _i64, _i64, _vp],

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "device_common.cuh"
 
@@ -660,6 +661,300 @@ __global__ void __launch_bounds__(256, DACSR_WSTREAM_MINB)
   cp_async_wait<0>();
 }
 
+// ------------------------------------------------- SLICED (lane per row)
+// The sliced layout (dacsr_slices_t): slice s = 32 rows, entry j of the
+// row in lane l at slot slice_ptr[s] + 32*j + l.  A warp takes one slice;
+// for each j the 32 lanes load one contiguous run of offsets and one of
+// values straight from HBM (fully coalesced, no shared-memory staging, no
+// per-chunk barrier), gather x at row + offset and fold in the exact naive
+// order.  Rows longer than the layout's max_len ("spill rows") are reduced
+// from the CSR arrays by the first side_ctas CTAs.
+template <class CI, class VT>
+struct SliceArgs {
+  const int64_t* __restrict__ ptr;
+  const uint8_t* __restrict__ len;
+  const CI* __restrict__ ci;
+  const VT* __restrict__ v;
+  int64_t row0, total;
+  int max_len;
+  // medium rows, 32 per medium slice
+  const int64_t* __restrict__ mrows;
+  const int64_t* __restrict__ mptr;
+  const CI* __restrict__ mci;
+  const VT* __restrict__ mv;
+  int64_t n_medium, m_nslices, m_total;
+  // long rows (warp per row)
+  const int64_t* __restrict__ lrows;
+  int64_t n_long;
+};
+
+// evict-first loads for the operator (read once per SpMV) so x stays in L2
+template <class T>
+__device__ __forceinline__ T ldcs(const T* p) {
+  return __ldcs(p);
+}
+template <>
+__device__ __forceinline__ int64_t ldcs<int64_t>(const int64_t* p) {
+  return static_cast<int64_t>(__ldcs(reinterpret_cast<const long long*>(p)));
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 ldcs<__nv_bfloat16>(const __nv_bfloat16* p) {
+  const unsigned short b = __ldcs(reinterpret_cast<const unsigned short*>(p));
+  return __ushort_as_bfloat16(b);
+}
+template <>
+__device__ __forceinline__ __half ldcs<__half>(const __half* p) {
+  const unsigned short b = __ldcs(reinterpret_cast<const unsigned short*>(p));
+  return __ushort_as_half(b);
+}
+
+// Long rows (listed ascending) inside [rs, re): one warp per row, exact
+// order (products staged per batch, lane 0 folds), from the CSR arrays.
+template <int KIND, class RP, class CI, class VT>
+__device__ __noinline__ void long_rows(const Mat<KIND, RP, CI, VT> m, Scal s, int64_t rs,
+                                       int64_t re, const int64_t* __restrict__ list,
+                                       int64_t n_list, int cta, int n_ctas, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(n_ctas) * (blockDim.x >> 5);
+  double* wscratch = scratch + (threadIdx.x >> 5) * 128;
+  for (int64_t w = static_cast<int64_t>(cta) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < n_list;
+       w += nw) {
+    const int64_t r = ldg(list + w);
+    if (r < rs || r >= re) continue;  // warp-uniform
+    const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1);
+    warp_long_row(m, s, r, b, e, static_cast<const VT*>(nullptr), static_cast<const CI*>(nullptr),
+                  0, 0, lane, wscratch);
+  }
+}
+
+// TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, multiple of 16)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// &base[off] as one IMAD.WIDE (32-bit signed offset scaled by the element
+// size into a 64-bit address) — the compiler otherwise sign-extends the
+// offset and forms the address with a 64-bit shift-add pair
+template <class VT>
+__device__ __forceinline__ const VT* elem_addr(const VT* base, int off) {
+  const VT* p;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(p) : "r"(off), "n"(static_cast<int>(sizeof(VT))), "l"(base));
+  return p;
+}
+template <class VT>
+__device__ __forceinline__ const VT* elem_addr(const VT* base, int64_t off) {
+  return base + off;
+}
+
+#ifndef DACSR_SLICED_MINB
+#define DACSR_SLICED_MINB 4
+#endif
+#ifndef DACSR_SLICED_BATCH
+#define DACSR_SLICED_BATCH 8
+#endif
+
+// One lane's row of a slice in the exact naive order.  li(j) / lv(j) load
+// entry j of the lane's row (offset / value) from wherever the slice sits
+// (HBM or the warp's shared-memory stage).  Slots past the lane's n load
+// nothing and contribute +0 * +0 = +0; acc + (+0) == acc bit-for-bit since
+// the naive sum from +0.0 never holds -0.0, so the fold needs no select.
+template <int B, class OT, int KIND, class RP, class CI, class VT, class LI, class LV>
+__device__ __forceinline__ double slice_row_dot(const Mat<KIND, RP, CI, VT>& m, int64_t r,
+                                                int width, int n, const VT* xr, const LI& li,
+                                                const LV& lv) {
+  double acc = 0.0;
+  for (int j = 0; j < width; j += B) {
+    OT o[B];
+    VT vv[B], xv[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const bool on = j + u < n;
+      o[u] = on ? static_cast<OT>(li(j + u)) : OT(0);
+      vv[u] = on ? lv(j + u) : VT(0);
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const bool on = j + u < n;
+      if (on) m.check(r, 0, static_cast<CI>(o[u]));
+      xv[u] = on ? ldg(elem_addr(xr, o[u])) : VT(0);
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, product(vv[u], xv[u]));
+  }
+  return acc;
+}
+
+// Per-warp staging of the sliced layout: kStages slots of one slice each
+// (values, then inner indices), slices up to `wcap` entries per lane.
+template <class CI, class VT>
+struct SliceStage {
+  static constexpr int kStages = 2;
+  __host__ __device__ static constexpr int value_bytes(int wcap) {
+    return 32 * wcap * static_cast<int>(sizeof(VT));
+  }
+  __host__ __device__ static constexpr int slot_bytes(int wcap) {
+    return value_bytes(wcap) + ((32 * wcap * static_cast<int>(sizeof(CI)) + 15) & ~15);
+  }
+  __host__ __device__ static constexpr int warp_bytes(int wcap) { return kStages * slot_bytes(wcap); }
+};
+
+// SLICED kernel.  Each warp first takes its share of the medium slices
+// (rows outside [rs, re) skipped lane by lane), then its main slices of
+// [rs, re); long rows go to the first side_ctas CTAs.  TMA == 0: every slice straight from HBM with
+// coalesced loads, the entries of the slice two steps ahead pulled into L2
+// by a bulk prefetch.  TMA == 1: each warp keeps the entries of its next
+// two slices in flight in its shared-memory stages (cp.async.bulk +
+// mbarrier, issued by lane 0), so only the x gathers sit in registers;
+// slices wider than wcap are read from HBM as in TMA == 0.
+template <int KIND, class RP, class CI, class VT, int TMA>
+__global__ void __launch_bounds__(256, DACSR_SLICED_MINB)
+    sliced_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs, int64_t re,
+                  int side_ctas, int wcap) {
+  constexpr int B = DACSR_SLICED_BATCH;
+  using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
+  using SS = SliceStage<CI, VT>;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  // programmatic dependent launch: metadata and operator loads may start
+  // while the previous grid drains; x / y only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (static_cast<int>(blockIdx.x) < side_ctas) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    long_rows(m, s, rs, re, sl.lrows, sl.n_long, blockIdx.x, side_ctas,
+              reinterpret_cast<double*>(dsm));
+    return;
+  }
+  __shared__ __align__(8) uint64_t bars[8][SS::kStages];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t W = static_cast<int64_t>(gridDim.x - side_ctas) * (blockDim.x >> 5);
+  const int64_t gw = static_cast<int64_t>(blockIdx.x - side_ctas) * (blockDim.x >> 5) + wib;
+  const int64_t s0 = (rs - sl.row0) >> 5, s1 = (re - sl.row0 + 31) >> 5;
+  const VT* __restrict__ xb = m.x + m.xoff;
+  bool waited = false;
+
+  // medium slices (few, up to medium_len wide): straight from HBM
+  for (int64_t t = gw; t < sl.m_nslices; t += W) {
+    const int64_t p0 = ldg(sl.mptr + t);
+    const int width = static_cast<int>((ldg(sl.mptr + t + 1) - p0) >> 5);
+    const int64_t k = 32 * t + lane;
+    int64_t r = -1;
+    int n = -1;
+    if (k < sl.n_medium) {
+      r = ldg(sl.mrows + k);
+      if (r >= rs && r < re) n = ldg(sl.len + (r - sl.row0));
+    }
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      waited = true;
+    }
+    const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
+    asm("" : "+l"(xr));
+    DACSR_CHECK(n <= width && width <= 254);
+    DACSR_CHECK(n <= 0 || p0 + lane + 32 * (n - 1) < sl.m_total);
+    const CI* pi = sl.mci + p0 + lane;
+    const VT* pv = sl.mv + p0 + lane;
+    const double acc = slice_row_dot<B, OT>(m, r, width, n, xr,
+                                            [&](int j) { return ldcs(pi + 32 * j); },
+                                            [&](int j) { return ldcs(pv + 32 * j); });
+    if (n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+  }
+
+  // main slices of [rs, re)
+  int64_t c = s0 + gw;
+  if (c >= s1) return;
+  unsigned char* wbase = dsm + (TMA ? wib * SS::warp_bytes(wcap) : 0);
+  uint64_t* bar = bars[wib];
+  if (TMA && lane == 0) {
+    for (int k = 0; k < SS::kStages; ++k) mbar_init(&bar[k], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  // slice metadata: raw loads now, arithmetic one iteration later (so the
+  // loads are never waited on where they are issued).  l: the lane's row
+  // length byte; 256 = not a row of this launch.
+  struct Raw {
+    int64_t a, b;
+    int l;
+  };
+  struct Meta {
+    int64_t p0;
+    int width, n;
+  };
+  auto load_raw = [&](int64_t cc) {
+    Raw w{0, 0, 256};
+    if (cc < s1) {
+      w.a = ldg(sl.ptr + cc);
+      w.b = ldg(sl.ptr + cc + 1);
+      const int64_t r = sl.row0 + 32 * cc + lane;
+      if (r >= rs && r < re) w.l = ldg(sl.len + (r - sl.row0));
+    }
+    return w;
+  };
+  auto derive = [&](const Raw& w) {
+    Meta q;
+    q.p0 = w.a;
+    q.width = static_cast<int>((w.b - w.a) >> 5);
+    q.n = w.l > sl.max_len ? -1 : w.l;  // 256 (none) or a medium / long row
+    return q;
+  };
+  auto is_staged = [&](const Meta& q) { return TMA && q.width > 0 && q.width <= wcap; };
+  // lane 0: the slice's two arrays into stage `slot` (TMA), or into L2
+  auto stage = [&](const Meta& q, int slot) {
+    if (lane != 0 || q.width <= 0) return;
+    const uint32_t vb = static_cast<uint32_t>(32 * q.width * sizeof(VT));
+    const uint32_t ib = static_cast<uint32_t>((32 * q.width * sizeof(CI) + 15) & ~size_t(15));
+    if (is_staged(q)) {
+      unsigned char* dst = wbase + slot * SS::slot_bytes(wcap);
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bar[slot], vb + ib);
+      bulk_copy_g2s(dst, sl.v + q.p0, vb, &bar[slot]);
+      bulk_copy_g2s(dst + SS::value_bytes(wcap), sl.ci + q.p0, ib, &bar[slot]);
+    } else {
+      prefetch_l2_bulk(sl.v + q.p0, vb);
+      prefetch_l2_bulk(sl.ci + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(CI)) & ~15u);
+    }
+  };
+  Meta cur = derive(load_raw(c));
+  Meta nxt = derive(load_raw(c + W));
+  if (TMA) stage(cur, 0);
+  stage(nxt, 1);
+  if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
+  uint32_t phase = 0;
+  for (int k = 0; c < s1; c += W, ++k) {
+    const int slot = k & 1;
+    const Raw raw2 = load_raw(c + 2 * W);
+    const int64_t r = sl.row0 + 32 * c + lane;
+    const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
+    // opaque base pointer: each gather is then one IMAD.WIDE off, xr
+    // instead of re-deriving x + (xoff + r + off) in 64-bit index space
+    asm("" : "+l"(xr));
+    DACSR_CHECK(cur.n <= cur.width && cur.width <= 254);
+    DACSR_CHECK(cur.n <= 0 || cur.p0 + lane + 32 * (cur.n - 1) < sl.total);
+    double acc;
+    if (is_staged(cur)) {
+      mbar_wait(&bar[slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      const unsigned char* base = wbase + slot * SS::slot_bytes(wcap);
+      const VT* pv = reinterpret_cast<const VT*>(base) + lane;
+      const CI* pi = reinterpret_cast<const CI*>(base + SS::value_bytes(wcap)) + lane;
+      acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
+                                 [&](int j) { return pi[32 * j]; },
+                                 [&](int j) { return pv[32 * j]; });
+    } else {
+      const CI* pi = sl.ci + cur.p0 + lane;
+      const VT* pv = sl.v + cur.p0 + lane;
+      acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
+                                 [&](int j) { return ldcs(pi + 32 * j); },
+                                 [&](int j) { return ldcs(pv + 32 * j); });
+    }
+    if (cur.n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+    __syncwarp();  // every lane is done with this slot before it is refilled
+    const Meta nxt2 = derive(raw2);
+    stage(nxt2, slot);
+    cur = nxt;
+    nxt = nxt2;
+  }
+}
+
 // planner: list the 32-row chunks that do not fit a VCAP window
 template <class RP>
 __global__ void classify_chunks_kernel(const RP* __restrict__ rp, int64_t rs, int64_t re,
@@ -715,6 +1010,9 @@ int sm_count() {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// the sliced arrays start 16-byte aligned (slices then start at multiples
+// of 32 entries, so every slice is a legal bulk-copy source)
+bool can_bulk_sl(const dacsr_slices_t* sd) { return aligned16(sd->values) && aligned16(sd->inner); }
 
 // Per-kernel launch configuration, computed once per (kernel, smem bytes):
 // the max-dynamic-smem attribute and the occupancy query cost microseconds
@@ -904,6 +1202,75 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
         return DACSR_ERR_CUDA;
       }
       return check_launch("wstream_kernel");
+    }
+    case DACSR_VARIANT_SLICED:
+    case DACSR_VARIANT_SLICED_TMA: {
+      const dacsr_plan_t* p = q.plan;
+      if (!p || !p->slices) return DACSR_ERR_PLAN;
+      const dacsr_slices_t* sd = p->slices;
+      if (q.rs < sd->row_start || q.re > sd->row_end || sd->max_len < 1 ||
+          sd->medium_len < sd->max_len || sd->medium_len > 254 || !sd->slice_ptr ||
+          !sd->row_len || (sd->total > 0 && (!sd->inner || !sd->values)) ||
+          (sd->n_medium > 0 && (!sd->medium_rows || !sd->m_slice_ptr ||
+                                (sd->m_total > 0 && (!sd->m_inner || !sd->m_values)))) ||
+          sd->m_nslices != ((sd->n_medium + 31) >> 5) || (sd->n_long > 0 && !sd->long_rows))
+        return DACSR_ERR_PLAN;
+      if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
+        // the sliced loop specialises the naive order; the others run row blocks
+        Req r2 = q;
+        r2.variant = p->block_rows && p->row_start == q.rs && p->row_end == q.re
+                         ? DACSR_VARIANT_ROWBLOCK
+                         : DACSR_VARIANT_STAGED;
+        return launch<KIND, RP, CI, VT>(a, r2);
+      }
+      SliceArgs<CI, VT> sa{sd->slice_ptr, sd->row_len, static_cast<const CI*>(sd->inner),
+                           static_cast<const VT*>(sd->values), sd->row_start, sd->total,
+                           sd->max_len, sd->medium_rows, sd->m_slice_ptr,
+                           static_cast<const CI*>(sd->m_inner), static_cast<const VT*>(sd->m_values),
+                           sd->n_medium, sd->m_nslices, sd->m_total, sd->long_rows, sd->n_long};
+      constexpr int warps = 8, threads = 32 * warps;
+      using SS = SliceStage<CI, VT>;
+      const bool tma = q.variant == DACSR_VARIANT_SLICED_TMA && can_bulk_sl(sd);
+      // stage width: the layout's longest kept row, within ~56 KiB of
+      // stages per CTA (4 CTAs per SM)
+      int wcap = 0;
+      if (tma) {
+        const int per_entry = 32 * SS::kStages * warps * static_cast<int>(sizeof(VT) + sizeof(CI));
+        wcap = std::max(1, std::min<int>(sd->max_len, (56 * 1024) / per_entry));
+      }
+      const size_t stage_bytes = tma ? static_cast<size_t>(warps) * SS::warp_bytes(wcap) : 0;
+      const size_t side_bytes = sd->n_long > 0 ? static_cast<size_t>(warps) * 128 * 8 : 0;
+      const size_t smem = std::max(stage_bytes, side_bytes);
+      auto kern = tma ? sliced_kernel<KIND, RP, CI, VT, 1> : sliced_kernel<KIND, RP, CI, VT, 0>;
+      int per_sm = cached_per_sm(kern, threads, smem);
+      if (per_sm < 0) return check_launch("sliced launch config");
+      if (p->ctas_per_sm > 0) per_sm = std::min(per_sm, static_cast<int>(p->ctas_per_sm));
+      const int64_t slots = static_cast<int64_t>(sms) * per_sm;
+      const int64_t nsl = ((q.re - sd->row_start + 31) >> 5) - ((q.rs - sd->row_start) >> 5) +
+                          sd->m_nslices;
+      // long rows: one warp each, at most 1/8 of the resident CTAs
+      const int side = sd->n_long > 0
+                           ? static_cast<int>(std::min<int64_t>((sd->n_long + warps - 1) / warps,
+                                                                std::max<int64_t>(1, slots / 8)))
+                           : 0;
+      const int64_t grid = std::min<int64_t>((nsl + warps - 1) / warps,
+                                             std::max<int64_t>(slots - side, slots / 2));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(grid, 1) + side));
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = q.stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, sa, q.rs, q.re, side, wcap);
+      if (e != cudaSuccess) {
+        set_last_error("sliced_kernel launch", e);
+        return DACSR_ERR_CUDA;
+      }
+      return check_launch("sliced_kernel");
     }
     default:
       return DACSR_ERR_VARIANT;

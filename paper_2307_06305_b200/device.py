@@ -78,6 +78,7 @@ class DeviceMatrix:
         self.plan = None
         self._block_rows = None
         self._chunk_plans = {}
+        self._sliced = None  # (plan, Slices, tensors) once build_slices ran
         self._launch_cache = {}
         self._spmv_fn = _native.lib().dacsr_spmv
         self.tuned_kernel = None
@@ -202,7 +203,126 @@ class DeviceMatrix:
             self._chunk_plans[None] = self._chunk_plans[key]
         return plan
 
-    def autotune(self, candidates=("wstream", "scalar", "rowblock", "staged"), cold=False,
+    # ---- sliced layout ------------------------------------------------------
+    def slice_max_len(self, quantiles=(0.5, 0.75, 0.9, 0.95, 0.98, 0.99, 0.995, 0.999, 1.0)):
+        """Longest row kept in the main slices: the candidate (a row-length
+        quantile, <= 254) minimising an estimate of the work — 32 slots per
+        unit of main-slice width, plus 2 per entry and 32 per row of the
+        longer rows (medium slices / warp-per-row)."""
+        rs, re = self.row_start, self.row_end
+        if re <= rs:
+            return 1
+        lens = (self.rowptr[rs + 1:re + 1].to(torch.int64) - self.rowptr[rs:re].to(torch.int64))
+        ns = (re - rs + 31) // 32
+        padded = torch.zeros(ns * 32, dtype=torch.int64, device=self.device)
+        padded[:re - rs] = lens
+        padded = padded.view(ns, 32)
+        qs = torch.quantile(lens.to(torch.float64)[:1 << 24],
+                            torch.tensor(quantiles, dtype=torch.float64, device=self.device))
+        cands = sorted({int(min(254, max(1, q))) for q in qs.ceil().tolist()})
+        best, best_cost = cands[-1], None
+        for t in cands:
+            keep = torch.where(padded <= t, padded, torch.zeros_like(padded))
+            out = padded > t
+            cost = (32 * keep.max(dim=1).values.sum() + 2 * padded[out].sum()
+                    + 32 * out.sum()).item()
+            if best_cost is None or cost < best_cost:
+                best, best_cost = t, cost
+        return best
+
+    def _scan(self, counts, out, sp):
+        """out[0] = 0, out[k+1] = sum(counts[:k+1]) (int64, on the device)."""
+        L = _native.lib()
+        n = counts.numel()
+        tb = ctypes.c_size_t(0)
+        _native.check(L.dacsr_counts_to_rowptr(
+            ctypes.c_void_p(counts.data_ptr()), n, ctypes.c_void_p(out.data_ptr()), _native.I64,
+            None, ctypes.byref(tb), sp), "dacsr_counts_to_rowptr")
+        tmp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=self.device)
+        _native.check(L.dacsr_counts_to_rowptr(
+            ctypes.c_void_p(counts.data_ptr()), n, ctypes.c_void_p(out.data_ptr()), _native.I64,
+            ctypes.c_void_p(tmp.data_ptr()), ctypes.byref(tb), sp), "dacsr_counts_to_rowptr")
+
+    def build_slices(self, max_len=None, medium_len=None, stream=None):
+        """Build the sliced device layout (dacsr_slices_t) of rows
+        [row_start, row_end): a bit-for-bit copy of the entries re-laid so a
+        warp reads entry j of its 32 rows as one contiguous run.  Rows up to
+        ``max_len`` entries sit in main slices, rows up to ``medium_len``
+        (default max(max_len, 32)) in medium slices of 32 listed rows, longer
+        rows are reduced warp by warp.  Returns the plan that carries it
+        (variants "sliced" / "sliced_tma")."""
+        L = _native.lib()
+        if self.plan is None:
+            self.build_plan(stream=stream)
+        if max_len is None:
+            max_len = self.slice_max_len()
+        max_len = int(min(254, max(1, max_len)))
+        medium_len = int(min(254, max(max_len, 32 if medium_len is None else medium_len)))
+        rs, re = self.row_start, self.row_end
+        ns = (re - rs + 31) // 32
+        dev = self.device
+        sp = _stream_ptr(stream)
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())
+        row_len = torch.empty(max(re - rs, 1), dtype=torch.uint8, device=dev)
+        counts = torch.zeros(3, max(ns, 1), dtype=torch.int32, device=dev)
+        ptrs = torch.zeros(3, ns + 1, dtype=torch.int64, device=dev)
+        with torch.cuda.device(dev):
+            _native.check(L.dacsr_slices_count(
+                ctypes.byref(self.desc), rs, re, max_len, medium_len, vp(row_len), vp(counts[0]),
+                vp(counts[1]), vp(counts[2]), sp), "dacsr_slices_count")
+            if ns:
+                for k in range(3):
+                    self._scan(counts[k, :ns], ptrs[k], sp)
+            total, n_medium, n_long = (int(v) for v in ptrs[:, -1].tolist())
+            inner = torch.empty(max(total, 1), dtype=self.colids.dtype, device=dev)
+            values = torch.empty(max(total, 1), dtype=self.values.dtype, device=dev)
+            medium_rows = torch.empty(max(n_medium, 1), dtype=torch.int64, device=dev)
+            long_rows = torch.empty(max(n_long, 1), dtype=torch.int64, device=dev)
+            msl = (n_medium + 31) // 32
+            m_ptr = torch.zeros(msl + 1, dtype=torch.int64, device=dev)
+            sl = _native.Slices(rs, re, ns, total, max_len, medium_len, ptrs[0].data_ptr(),
+                                row_len.data_ptr(), inner.data_ptr(), values.data_ptr(),
+                                n_medium, msl, 0, medium_rows.data_ptr(), m_ptr.data_ptr(),
+                                None, None, n_long, long_rows.data_ptr())
+            _native.check(L.dacsr_slices_fill(ctypes.byref(self.desc), ctypes.byref(sl),
+                                              vp(ptrs[1]), vp(ptrs[2]), sp), "dacsr_slices_fill")
+            m_inner = m_values = None
+            if n_medium:
+                m_counts = torch.empty(msl, dtype=torch.int32, device=dev)
+                _native.check(L.dacsr_slices_medium_count(ctypes.byref(sl), vp(m_counts), sp),
+                              "dacsr_slices_medium_count")
+                self._scan(m_counts, m_ptr, sp)
+                m_total = int(m_ptr[-1].item())
+                m_inner = torch.empty(max(m_total, 1), dtype=self.colids.dtype, device=dev)
+                m_values = torch.empty(max(m_total, 1), dtype=self.values.dtype, device=dev)
+                sl.m_total, sl.m_inner, sl.m_values = m_total, m_inner.data_ptr(), m_values.data_ptr()
+                _native.check(L.dacsr_slices_medium_fill(ctypes.byref(self.desc), ctypes.byref(sl),
+                                                         sp), "dacsr_slices_medium_fill")
+        plan = _native.Plan()
+        ctypes.memmove(ctypes.byref(plan), ctypes.byref(self.plan), ctypes.sizeof(plan))
+        plan.slices = ctypes.addressof(sl)
+        plan.ctas_per_sm = getattr(self, "_ctas_per_sm", 0)
+        tensors = {"row_len": row_len, "slice_ptr": ptrs[0], "inner": inner, "values": values,
+                   "medium_rows": medium_rows, "m_slice_ptr": m_ptr, "m_inner": m_inner,
+                   "m_values": m_values, "long_rows": long_rows}
+        self._sliced = (plan, sl, tensors)
+        self._launch_cache.clear()
+        return plan
+
+    def slices_info(self):
+        """Summary of the sliced layout (None before build_slices)."""
+        if self._sliced is None:
+            return None
+        _, sl, tensors = self._sliced
+        return {"max_len": sl.max_len, "medium_len": sl.medium_len, "slots": sl.total,
+                "n_medium": sl.n_medium, "m_slots": sl.m_total, "n_long": sl.n_long,
+                "nslices": sl.nslices,
+                "padding": (sl.total + sl.m_total) / max(1, self.nnz) - 1.0,
+                "bytes": sum(t.numel() * t.element_size() for t in tensors.values()
+                             if t is not None)}
+
+    def autotune(self, candidates=("sliced", "sliced_tma", "wstream", "scalar", "rowblock",
+                                   "staged"), cold=False,
                  x=None, reps=5):
         """Time the exact naive-order kernels on this matrix and remember the
         fastest for variant "naive"/"auto" (all give bit-identical results,
@@ -213,7 +333,7 @@ class DeviceMatrix:
         y = torch.empty(self.nrows, dtype=self.values.dtype, device=self.device)
         times = {}
         for k in candidates:
-            if k in ("wstream", "rowblock") and self.plan is None:
+            if k in ("wstream", "rowblock", "sliced", "sliced_tma") and self.plan is None:
                 continue
             fn = lambda k=k: self.spmv_into(x, y, 1.0, 0.0, k, 0)
             times[k] = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
@@ -225,6 +345,8 @@ class DeviceMatrix:
         """Cap WSTREAM's resident CTAs per SM (0 = occupancy maximum)."""
         for plan, _ in self._chunk_plans.values():
             plan.ctas_per_sm = int(n)
+        if self._sliced is not None:
+            self._sliced[0].ctas_per_sm = int(n)
         self._ctas_per_sm = int(n)
         self._launch_cache.clear()
 
@@ -241,6 +363,10 @@ class DeviceMatrix:
         differs from the planned one)."""
         rs = self.row_start if row_start is None else row_start
         re = self.row_end if row_end is None else row_end
+        if kname in ("sliced", "sliced_tma"):  # the slices serve any row range inside theirs
+            if not (self.row_start <= rs <= re <= self.row_end):
+                return None
+            return self._sliced[0] if self._sliced is not None else self.build_slices()
         if self.plan is None or rs != self.plan.row_start or re != self.plan.row_end:
             return None
         if kname == "wstream":

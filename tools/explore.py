@@ -43,6 +43,9 @@ def run(name, mats, x):
                 continue
             if kname == "wstream":
                 v += f"[vcap={dm.chunk_plan().chunk_vcap},cx={dm.chunk_plan().n_complex}]"
+            if kname == "sliced":
+                inf = dm.slices_info()
+                v += f"[T={inf['max_len']},pad={inf['padding']:.3f},med={inf['n_medium']},long={inf['n_long']}]"
             rec = dict(config=name, kind=kind, variant=v, us=t * 1e6, gbs=tr / t / 1e9,
                        bytes=tr, cold=args.cold, plan_cap=dm.plan.cap if dm.plan else None)
             out.append(rec)
@@ -51,7 +54,12 @@ def run(name, mats, x):
 
 for c in args.configs.split(","):
     t0 = time.time()
-    if c in ("c1", "c2", "c2f32"):
+    if c == "c2bf16":
+        csr = laplacian_3d(128)
+        mats = {k: DeviceMatrix.from_host(a).astype(torch.bfloat16)
+                for k, a in (("csr", csr), ("da", dg.to_dacsr(csr, 16)))}
+        x = torch.from_numpy(uniform_x(csr.ncols, 1)).to(dev).to(torch.bfloat16)
+    elif c in ("c1", "c2", "c2f32"):
         dt = np.float32 if c == "c2f32" else np.float64
         csr = laplacian_2d(1024, dt) if c == "c1" else laplacian_3d(128, dt)
         mats = {"csr": DeviceMatrix.from_host(csr), "da": DeviceMatrix.from_host(dg.to_dacsr(csr, 16))}
