@@ -192,6 +192,11 @@ def measure_device(dm, x, variant, steps, warmup, per_step=SPMV_PER_STEP):
     from paper_2307_06305_b200.harness import GraphBatch, flush_l2
     from paper_2307_06305_b200.spmv import kernel_for, resolve_variant
     kname, order = resolve_variant(variant)
+    tuned = None
+    if variant == "naive":
+        # every exact kernel gives the same bits; run the fastest one in the
+        # regime measured here (back-to-back SpMVs)
+        tuned = {k: round(v * 1e6, 2) for k, v in dm.autotune(x=x, reps=20).items()}
     kname = kernel_for(dm, kname, order)
     y = torch.empty(dm.nrows, dtype=dm.values.dtype, device=dm.device)
     g = GraphBatch(lambda: dm.spmv_into(x, y, 1.0, 0.0, kname, order), per_step)
@@ -207,7 +212,7 @@ def measure_device(dm, x, variant, steps, warmup, per_step=SPMV_PER_STEP):
         e1.record()
         e1.synchronize()
         cold.append(e0.elapsed_time(e1) / 1e3)
-    return kname, order, times, sorted(cold)[len(cold) // 2], y
+    return kname, order, times, sorted(cold)[len(cold) // 2], y, tuned
 
 
 def measure_e2e(a_host, x, steps, warmup, per_step):
@@ -392,8 +397,8 @@ def run_ours(args):
     x = torch.from_numpy(xh).to(dev)
 
     with ClockSampler(local) as clocks:
-        kname, order, times, cold_da, y = measure_device(dm, x, args.variant, args.steps,
-                                                         args.warmup)
+        kname, order, times, cold_da, y, tuned = measure_device(dm, x, args.variant, args.steps,
+                                                                args.warmup)
     step_s = sum(times) / len(times)
     value = SPMV_PER_STEP * t_da * len(times) / sum(times) / 1e9
     # parity spot check of the benchmarked result (rows sampled vs oracle)
@@ -402,8 +407,8 @@ def run_ours(args):
     yref = oracle.spmv("da", da.rowptr, da.colids, da.values, xh, threads=8)
     parity = bool(np.array_equal(y.cpu().numpy().view(np.uint64), yref.view(np.uint64)))
 
-    kc, _, times_c, cold_csr, _ = measure_device(dmc, x, args.variant, max(3, args.steps // 2),
-                                                 2)
+    kc, _, times_c, cold_csr, _, _ = measure_device(dmc, x, args.variant,
+                                                    max(3, args.steps // 2), 2)
     step_c = sum(times_c) / len(times_c)
 
     e2e_step, _ = measure_e2e(da, xh, max(2, args.steps // 5), 1, SPMV_PER_STEP // 10)
@@ -421,6 +426,8 @@ def run_ours(args):
         "config": {"workload": "C2: 3D 7-pt Laplacian 128^3 (n=2097152, nnz=14581760), DA-CSR "
                                "i16 offsets, f64, x~U[-1,1] seed 1",
                    "spmv_per_step": SPMV_PER_STEP, "kernel": kname,
+                   "kernel_selection": "fastest exact kernel (bit-identical results), warm "
+                                       "autotune in us per SpMV: " + json.dumps(tuned),
                    "l2": "188 MB matrix > 126 MB L2; L2 flushed (read of 2x L2, clean lines) before every step",
                    "parallelism": "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

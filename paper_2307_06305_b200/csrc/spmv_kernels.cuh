@@ -752,6 +752,12 @@ __device__ __forceinline__ const VT* elem_addr(const VT* base, int64_t off) {
 #ifndef DACSR_SLICED_BATCH
 #define DACSR_SLICED_BATCH 8
 #endif
+#ifndef DACSR_SLICED_PREFETCH
+#define DACSR_SLICED_PREFETCH 1
+#endif
+#ifndef DACSR_SLICED_LDCS
+#define DACSR_SLICED_LDCS 1
+#endif
 
 // One lane's row of a slice in the exact naive order.  li(j) / lv(j) load
 // entry j of the lane's row (offset / value) from wherever the slice sits
@@ -908,7 +914,7 @@ __global__ void __launch_bounds__(256, DACSR_SLICED_MINB)
       mbar_arrive_expect_tx(&bar[slot], vb + ib);
       bulk_copy_g2s(dst, sl.v + q.p0, vb, &bar[slot]);
       bulk_copy_g2s(dst + SS::value_bytes(wcap), sl.ci + q.p0, ib, &bar[slot]);
-    } else {
+    } else if (DACSR_SLICED_PREFETCH) {
       prefetch_l2_bulk(sl.v + q.p0, vb);
       prefetch_l2_bulk(sl.ci + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(CI)) & ~15u);
     }
@@ -942,9 +948,14 @@ __global__ void __launch_bounds__(256, DACSR_SLICED_MINB)
     } else {
       const CI* pi = sl.ci + cur.p0 + lane;
       const VT* pv = sl.v + cur.p0 + lane;
-      acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
-                                 [&](int j) { return ldcs(pi + 32 * j); },
-                                 [&](int j) { return ldcs(pv + 32 * j); });
+      if (DACSR_SLICED_LDCS)
+        acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
+                                   [&](int j) { return ldcs(pi + 32 * j); },
+                                   [&](int j) { return ldcs(pv + 32 * j); });
+      else
+        acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
+                                   [&](int j) { return ldg(pi + 32 * j); },
+                                   [&](int j) { return ldg(pv + 32 * j); });
     }
     if (cur.n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
     __syncwarp();  // every lane is done with this slot before it is refilled

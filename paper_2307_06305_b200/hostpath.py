@@ -60,17 +60,28 @@ class StreamedHost:
         key = (kname, order)
         rec = self._plans.get(key)
         if rec is None:
-            kernels = [kernel_for(v, kname, order) for v in self.views]
-            if len(set(kernels)) != 1:
-                kernels = ["staged"] * len(self.views)
-            k = kernels[0]
+            k = kernel_for(self.dm, kname, order)
             plans = (_native.Plan * len(self.views))()
-            for i, v in enumerate(self.views):
-                pl = v.plan_for(k)
-                if pl is None:  # plan-free kernel: row range only
-                    plans[i].row_start, plans[i].row_end = v.row_start, v.row_end
-                else:
+            if k in ("sliced", "sliced_tma"):
+                # the pieces share the whole matrix's sliced layout (the
+                # kernel takes any row range inside it); no row-block table
+                pl = self.dm.plan_for(k)
+                for i, v in enumerate(self.views):
                     ctypes.memmove(ctypes.byref(plans[i]), ctypes.byref(pl), ctypes.sizeof(pl))
+                    plans[i].row_start, plans[i].row_end = v.row_start, v.row_end
+                    plans[i].block_rows = None
+            else:
+                kernels = [kernel_for(v, kname, order) for v in self.views]
+                if len(set(kernels)) != 1:
+                    kernels = ["staged"] * len(self.views)
+                k = kernels[0]
+                for i, v in enumerate(self.views):
+                    pl = v.plan_for(k)
+                    if pl is None:  # plan-free kernel: row range only
+                        plans[i].row_start, plans[i].row_end = v.row_start, v.row_end
+                    else:
+                        ctypes.memmove(ctypes.byref(plans[i]), ctypes.byref(pl),
+                                       ctypes.sizeof(pl))
             rec = (plans, _native.VARIANT_CODES[k])
             self._plans[key] = rec
         plans, code = rec

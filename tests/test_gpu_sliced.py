@@ -135,3 +135,22 @@ def test_skewed_spill_rows_full_size(cuda):
         assert np.array_equal(bits(got.cpu().numpy()), bits(ref)), variant
     info = dm.slices_info()
     assert info["n_medium"] > 0 and info["n_long"] > 0
+
+
+@pytest.mark.parametrize("variant", ["sliced", "sliced_tma"])
+def test_streamed_host_path_on_slices(cuda, variant):
+    """spmv(A, x_host, y_host) with the slices: the row pieces of the
+    streamed host path share the whole matrix's layout; bit-exact."""
+    a = dg.to_dacsr(add_skew_rows(laplacian_2d(512), frac=0.01, alpha=1.5, cap=600, band=500,
+                                  seed=3), 16)
+    dm = DeviceMatrix.of(a)
+    dm.build_slices(5, 32)
+    dm.tuned_kernel = variant
+    x = uniform_x(a.ncols, 4)
+    for alpha, beta in ((1.0, 0.0), (0.5, -2.0)):
+        y0 = np.random.default_rng(1).uniform(-1, 1, a.nrows)
+        y = y0.copy()
+        dg.spmv(a, x, y, alpha, beta)
+        ref = oracle.spmv("da", a.rowptr, a.colids, a.values, x, y0.copy(), alpha, beta)
+        assert np.array_equal(bits(y), bits(ref)), (alpha, beta)
+    dm.tuned_kernel = None
