@@ -68,13 +68,14 @@ def peaks():
 
 
 def ncu_traffic(kernel_key):
-    """dram bytes per launch from the committed ncu summary, if present."""
+    """(dram bytes per launch, note) from the committed ncu summary, if present."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel_key, {}).get("dram_bytes_per_launch")
+            rec = json.load(f).get(kernel_key, {})
+        return rec.get("dram_bytes_per_launch"), rec.get("note")
     except (OSError, ValueError):
-        return None
+        return None, None
 
 
 def c2_host(dtype=np.float64):
@@ -418,6 +419,7 @@ def run_ours(args):
     peak, peak_src = peaks()
     per_launch = step_s / SPMV_PER_STEP
     achieved = t_da / per_launch / 1e9
+    traffic, traffic_note = ncu_traffic(kname + ":c2:da")
     line = {
         "metric": "SpMV effective HBM GB/s (DA-CSR i16, f64)",
         "value": round(value, 1), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
@@ -431,7 +433,10 @@ def run_ours(args):
                    "l2": "188 MB matrix > 126 MB L2; L2 flushed (read of 2x L2, clean lines) before every step",
                    "parallelism": "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(kname + ":c2:da"),
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_note": traffic_note,
+                     "dram_gbs_at_traffic": (round(traffic / per_launch / 1e9, 1)
+                                             if traffic else None),
                      "peak_source": peak_src, "bytes_per_launch": t_da,
                      "frac_of_nominal_8TBs": round(achieved / 8000.0, 4),
                      "frac_of_tma_read_ceiling": round(achieved / READ_CEILING_GBS, 4),

@@ -759,6 +759,7 @@ __device__ __forceinline__ const VT* elem_addr(const VT* base, int64_t off) {
 #define DACSR_SLICED_LDCS 1
 #endif
 
+
 // One lane's row of a slice in the exact naive order.  li(j) / lv(j) load
 // entry j of the lane's row (offset / value) from wherever the slice sits
 // (HBM or the warp's shared-memory stage).  Slots past the lane's n load
@@ -767,9 +768,8 @@ __device__ __forceinline__ const VT* elem_addr(const VT* base, int64_t off) {
 template <int B, class OT, int KIND, class RP, class CI, class VT, class LI, class LV>
 __device__ __forceinline__ double slice_row_dot(const Mat<KIND, RP, CI, VT>& m, int64_t r,
                                                 int width, int n, const VT* xr, const LI& li,
-                                                const LV& lv) {
-  double acc = 0.0;
-  for (int j = 0; j < width; j += B) {
+                                                const LV& lv, int j0 = 0, double acc = 0.0) {
+  for (int j = j0; j < width; j += B) {
     OT o[B];
     VT vv[B], xv[B];
 #pragma unroll
@@ -867,9 +867,9 @@ __global__ void __launch_bounds__(256, DACSR_SLICED_MINB)
   // main slices of [rs, re)
   int64_t c = s0 + gw;
   if (c >= s1) return;
-  unsigned char* wbase = dsm + (TMA ? wib * SS::warp_bytes(wcap) : 0);
+  unsigned char* wbase = dsm + (TMA == 1 ? wib * SS::warp_bytes(wcap) : 0);
   uint64_t* bar = bars[wib];
-  if (TMA && lane == 0) {
+  if (TMA == 1 && lane == 0) {
     for (int k = 0; k < SS::kStages; ++k) mbar_init(&bar[k], 1);
     mbar_fence_init();
   }
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(256, DACSR_SLICED_MINB)
     q.n = w.l > sl.max_len ? -1 : w.l;  // 256 (none) or a medium / long row
     return q;
   };
-  auto is_staged = [&](const Meta& q) { return TMA && q.width > 0 && q.width <= wcap; };
+  auto is_staged = [&](const Meta& q) { return TMA == 1 && q.width > 0 && q.width <= wcap; };
   // lane 0: the slice's two arrays into stage `slot` (TMA), or into L2
   auto stage = [&](const Meta& q, int slot) {
     if (lane != 0 || q.width <= 0) return;
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(256, DACSR_SLICED_MINB)
   };
   Meta cur = derive(load_raw(c));
   Meta nxt = derive(load_raw(c + W));
-  if (TMA) stage(cur, 0);
+  if (TMA == 1) stage(cur, 0);
   stage(nxt, 1);
   if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
   uint32_t phase = 0;

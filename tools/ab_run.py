@@ -49,7 +49,12 @@ for c in configs:
         fn = lambda: dm.spmv_into(x, y, 1.0, 0.0, variant, 0)
         warm = time_kernel(fn, epochs=5, warmup_iters=3, min_epoch_iters=3, min_epoch_time=0.05, graph=50)
         cold = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=8, min_epoch_time=0.0, cold=True)
-        print(json.dumps({"lib": tag, "config": c, "kind": kind, "variant": variant,
+        y2 = torch.empty_like(y)
+        dm.spmv_into(x, y2, 1.0, 0.0, "scalar", 0)
+        fn()
+        exact = bool(torch.equal(y.view(torch.int16) if y.element_size() == 2 else y.view(torch.int32 if y.element_size() == 4 else torch.int64),
+                                 y2.view(torch.int16) if y.element_size() == 2 else y2.view(torch.int32 if y.element_size() == 4 else torch.int64)))
+        print(json.dumps({"lib": tag, "config": c, "kind": kind, "variant": variant, "exact": exact,
                           "warm_us": round(warm * 1e6, 2), "warm_gbs": round(tr / warm / 1e9),
                           "cold_us": round(cold * 1e6, 2), "cold_gbs": round(tr / cold / 1e9)}), flush=True)
     del mats
