@@ -27,8 +27,9 @@ def test_sumsq_matches_oracle_restatement(cuda):
     assert float(fold_ordered(p).item()) == oracle.fold_ordered(want)
 
 
+@pytest.mark.parametrize("variant", ["naive", "sliced"])
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_rank_local_blocks_bit_exact(cuda, world):
+def test_rank_local_blocks_bit_exact(cuda, world, variant):
     arr = banded_arrays(N, B, LAM, KMAX, SEED, cuda, kinds=("da", "csr"))
     full = DeviceMatrix("da", N, N, arr["rowptr"], arr["offsets"], arr["values"])
     x = normal_vector(N, 9, cuda)
@@ -42,7 +43,8 @@ def test_rank_local_blocks_bit_exact(cuda, world):
         loc = banded_arrays(N, B, LAM, KMAX, SEED, cuda, r0=r0, r1=r1, kinds=("da", "csr"))
         x_ext = x[plan.lo:plan.hi].clone()        # what the halo exchange delivers
         for kind, inner in (("da", "offsets"), ("csr", "colids")):
-            op = D.CudaLocalOp(kind, loc["rowptr"], loc[inner], loc["values"], N, plan, 1024, B)
+            op = D.CudaLocalOp(kind, loc["rowptr"], loc[inner], loc["values"], N, plan, 1024, B,
+                               variant=variant)
             y = torch.empty(r1 - r0, dtype=torch.float64, device=cuda)
             for which in range(3):
                 op.spmv_part(which, x_ext, y, 0.75)
@@ -107,7 +109,7 @@ def test_nnz_above_2_31_int64_rowptr(cuda):
     rng = np.random.default_rng(2)
     rows = np.concatenate([[0, n - 1, n // 2], rng.integers(n - (1 << 20), n, 40),
                            rng.integers(0, n, 40)])
-    for kernel in ("wstream", "rowblock"):
+    for kernel in ("wstream", "rowblock", "sliced"):
         y = torch.empty(n, dtype=torch.float64, device=cuda)
         dm.spmv_into(x, y, 1.0, 0.0, kernel, 0)
         for r in rows.tolist():
