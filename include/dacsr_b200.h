@@ -235,8 +235,11 @@ int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t varian
  * the row ranges of plans[0..npieces) (ascending, covering the rows); piece
  * p needs x[0, min(ncols, row_end_p + w)) with w the bandwidth (max |col -
  * row|).  x_dev / y_dev are caller-owned device buffers of ncols / nrows
- * values; the three streams carry H2D copies, kernels and D2H copies.
- * Blocks until y_host is complete.  Host buffers should be pinned. */
+ * values; s_h2d carries the x copies, s_comp the kernels.  If y_host is
+ * page-locked and mapped (cudaHostAlloc / cudaHostRegister under UVA) the
+ * kernels store y straight into it over PCIe and y_dev / s_d2h are unused;
+ * otherwise y returns through y_dev with D2H copies on s_d2h.  Blocks until
+ * y_host is complete. */
 int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans, int32_t npieces,
                              int32_t variant, int32_t order, const void* x_host, void* y_host,
                              void* x_dev, void* y_dev, double alpha, double beta, int64_t w,

@@ -137,9 +137,13 @@ int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t varian
 
 // Host-buffer SpMV with the copies overlapped (see hostpath.py): rows are
 // split into the plans' row ranges; piece p needs x[0, min(ncols, r1_p + w))
-// (w = bandwidth).  h2d: the x prefix not yet sent (+ the y piece if
-// beta != 0); comp: waits for it, runs the piece; d2h: waits for the piece,
-// copies its y rows back.  Blocks until y_host is complete.
+// (w = bandwidth).  h2d: the x prefix not yet sent; comp: waits for it, runs
+// the piece.  y: when y_host is page-locked and mapped (any cudaHostAlloc /
+// registered buffer under UVA) the kernels store y straight into host
+// memory over PCIe — the D2H copy disappears and with it the pipeline drain
+// (and with beta != 0 they read the old y from there too).  Otherwise y goes
+// through y_dev: the y piece in on h2d if beta != 0, out on d2h after the
+// piece's kernel.  Blocks until y_host is complete.
 int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans, int32_t npieces,
                              int32_t variant, int32_t order, const void* x_host, void* y_host,
                              void* x_dev, void* y_dev, double alpha, double beta, int64_t w,
@@ -152,6 +156,16 @@ int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans,
   const size_t vb = kBytes[a->values_dtype];
   auto h2d = static_cast<cudaStream_t>(s_h2d), comp = static_cast<cudaStream_t>(s_comp),
        d2h = static_cast<cudaStream_t>(s_d2h);
+  // y straight to host memory?
+  void* y_mapped = nullptr;
+  {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, y_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer)
+      y_mapped = pa.devicePointer;
+    else
+      cudaGetLastError();  // pageable memory: not an error, take the copy path
+  }
   cudaEvent_t ev[128];
   int nev = 0;
   auto fail = [&](const char* what, cudaError_t e) {
@@ -168,6 +182,7 @@ int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans,
   char* yh = static_cast<char*>(y_host);
   char* xd = static_cast<char*>(x_dev);
   char* yd = static_cast<char*>(y_dev);
+  void* y_target = y_mapped ? y_mapped : y_dev;
   int64_t sent = 0;
   cudaError_t e;
   for (int p = 0; p < npieces; ++p) {
@@ -179,20 +194,21 @@ int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans,
       if (e != cudaSuccess) return fail("streamed x copy", e);
       sent = hi;
     }
-    if (beta != 0.0 && r1 > r0) {
+    if (!y_mapped && beta != 0.0 && r1 > r0) {
       e = cudaMemcpyAsync(yd + r0 * vb, yh + r0 * vb, (r1 - r0) * vb, cudaMemcpyHostToDevice, h2d);
       if (e != cudaSuccess) return fail("streamed y copy in", e);
     }
     if ((e = cudaEventRecord(ev[2 * p], h2d)) != cudaSuccess) return fail("event", e);
     if ((e = cudaStreamWaitEvent(comp, ev[2 * p], 0)) != cudaSuccess) return fail("wait", e);
     if (r1 > r0) {
-      const int rc = dacsr_spmv(a, &plans[p], variant, order, x_dev, 0, y_dev, alpha, beta, r0, r1,
-                                s_comp);
+      const int rc = dacsr_spmv(a, &plans[p], variant, order, x_dev, 0, y_target, alpha, beta, r0,
+                                r1, s_comp);
       if (rc) {
         for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
         return rc;
       }
     }
+    if (y_mapped) continue;
     if ((e = cudaEventRecord(ev[2 * p + 1], comp)) != cudaSuccess) return fail("event", e);
     if ((e = cudaStreamWaitEvent(d2h, ev[2 * p + 1], 0)) != cudaSuccess) return fail("wait", e);
     if (r1 > r0) {
@@ -200,7 +216,7 @@ int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans,
       if (e != cudaSuccess) return fail("streamed y copy out", e);
     }
   }
-  e = cudaStreamSynchronize(d2h);
+  e = cudaStreamSynchronize(y_mapped ? comp : d2h);
   for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
   if (e != cudaSuccess) {
     set_last_error("streamed sync", e);

@@ -758,6 +758,9 @@ __device__ __forceinline__ const VT* elem_addr(const VT* base, int64_t off) {
 #ifndef DACSR_SLICED_LDCS
 #define DACSR_SLICED_LDCS 1
 #endif
+#ifndef DACSR_SLICED_LATE_VALUES
+#define DACSR_SLICED_LATE_VALUES 0
+#endif
 
 
 // One lane's row of a slice in the exact naive order.  li(j) / lv(j) load
@@ -776,13 +779,20 @@ __device__ __forceinline__ double slice_row_dot(const Mat<KIND, RP, CI, VT>& m, 
     for (int u = 0; u < B; ++u) {
       const bool on = j + u < n;
       o[u] = on ? static_cast<OT>(li(j + u)) : OT(0);
-      vv[u] = on ? lv(j + u) : VT(0);
+      if (!DACSR_SLICED_LATE_VALUES) vv[u] = on ? lv(j + u) : VT(0);
     }
 #pragma unroll
     for (int u = 0; u < B; ++u) {
       const bool on = j + u < n;
       if (on) m.check(r, 0, static_cast<CI>(o[u]));
       xv[u] = on ? ldg(elem_addr(xr, o[u])) : VT(0);
+    }
+    if (DACSR_SLICED_LATE_VALUES) {
+      // values after the gathers: the offsets are dead by then, so the
+      // batch peaks at 2 x B values instead of 2.5 x B (same latency: the
+      // values, prefetched into L2, arrive alongside the gathers)
+#pragma unroll
+      for (int u = 0; u < B; ++u) vv[u] = j + u < n ? lv(j + u) : VT(0);
     }
 #pragma unroll
     for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, product(vv[u], xv[u]));

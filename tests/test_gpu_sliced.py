@@ -147,10 +147,14 @@ def test_streamed_host_path_on_slices(cuda, variant):
     dm.build_slices(5, 32)
     dm.tuned_kernel = variant
     x = uniform_x(a.ncols, 4)
+    yp = torch.empty(a.nrows, dtype=torch.float64, pin_memory=True)
     for alpha, beta in ((1.0, 0.0), (0.5, -2.0)):
         y0 = np.random.default_rng(1).uniform(-1, 1, a.nrows)
-        y = y0.copy()
-        dg.spmv(a, x, y, alpha, beta)
         ref = oracle.spmv("da", a.rowptr, a.colids, a.values, x, y0.copy(), alpha, beta)
+        y = y0.copy()                      # pageable: y through the device + D2H
+        dg.spmv(a, x, y, alpha, beta)
         assert np.array_equal(bits(y), bits(ref)), (alpha, beta)
+        yp.numpy()[:] = y0                 # pinned: the kernels store y in host memory
+        dg.spmv(a, x, yp.numpy(), alpha, beta)
+        assert np.array_equal(bits(yp.numpy()), bits(ref)), (alpha, beta, "pinned")
     dm.tuned_kernel = None
