@@ -1234,7 +1234,8 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
           !sd->row_len || (sd->total > 0 && (!sd->inner || !sd->values)) ||
           (sd->n_medium > 0 && (!sd->medium_rows || !sd->m_slice_ptr ||
                                 (sd->m_total > 0 && (!sd->m_inner || !sd->m_values)))) ||
-          sd->m_nslices != ((sd->n_medium + 31) >> 5) || (sd->n_long > 0 && !sd->long_rows))
+          sd->m_nslices != ((sd->n_medium + 31) >> 5) || (sd->n_long > 0 && !sd->long_rows) ||
+          sd->row_end - sd->row_start >= (int64_t(1) << 31))  // rows kept as int32 offsets
         return DACSR_ERR_PLAN;
       if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
         // the sliced loop specialises the naive order; the others run row blocks

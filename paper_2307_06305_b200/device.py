@@ -259,6 +259,8 @@ class DeviceMatrix:
         max_len = int(min(254, max(1, max_len)))
         medium_len = int(min(254, max(max_len, 32 if medium_len is None else medium_len)))
         rs, re = self.row_start, self.row_end
+        if re - rs >= 1 << 31:
+            raise ValueError("the sliced layout addresses rows as int32 offsets (< 2^31 rows)")
         ns = (re - rs + 31) // 32
         dev = self.device
         sp = _stream_ptr(stream)
