@@ -437,6 +437,8 @@ def run_ours(args):
                      "traffic_note": traffic_note,
                      "dram_gbs_at_traffic": (round(traffic / per_launch / 1e9, 1)
                                              if traffic else None),
+                     "dram_frac_at_traffic": (round(traffic / per_launch / 1e9 / peak, 4)
+                                              if traffic else None),
                      "peak_source": peak_src, "bytes_per_launch": t_da,
                      "frac_of_nominal_8TBs": round(achieved / 8000.0, 4),
                      "frac_of_tma_read_ceiling": round(achieved / READ_CEILING_GBS, 4),

@@ -320,8 +320,11 @@ def bench_main(args, rank, world, local):
     bufs[0][own] = x
     # the exact kernels give the same bits: time each on the real distributed
     # step (max over ranks) and keep the fastest everywhere
+    # (graph capture of NCCL P2P is only attempted at one rank here: a failed
+    # capture on a multi-rank communicator is not worth the risk before the
+    # timed run; at N > 1 the kernel measured fastest at one rank is used)
     tuned = {}
-    for cand in ("sliced", "wstream"):
+    for cand in (("sliced", "wstream") if world == 1 else ("sliced",)):
         op = CudaLocalOp("da", t_rp, t_off, t_val, n, plan, 1 << 16, plane, variant=cand)
         def burst(op=op):
             for _ in range(20):

@@ -52,3 +52,28 @@ def test_arg_validation_without_device():
     st = _native.Stats(4, 5, 0, 5, 2, 0, 1.25, 0.3)
     cap = L.dacsr_plan_default_cap(ctypes.byref(st), _native.F64, _native.I16)
     assert cap % 16 == 0 and cap >= 512
+
+
+def test_slices_arg_validation_without_device():
+    """The sliced-layout builder rejects bad arguments before any CUDA call."""
+    L = _native.lib()
+    m = _native.Matrix(_native.KIND_DA, _native.I32, _native.I16, _native.F64, 64, 64, 100,
+                       None, None, None)
+    # null rowptr / bad max_len / medium_len < max_len / bad row range
+    assert L.dacsr_slices_count(ctypes.byref(m), 0, 64, 4, 8, None, None, None, None, None) == 1
+    m.rowptr = 16
+    assert L.dacsr_slices_count(ctypes.byref(m), 0, 64, 0, 8, None, None, None, None, None) == 1
+    assert L.dacsr_slices_count(ctypes.byref(m), 0, 64, 9, 8, None, None, None, None, None) == 1
+    assert L.dacsr_slices_count(ctypes.byref(m), 0, 65, 4, 8, None, None, None, None, None) == 1
+    assert L.dacsr_slices_count(ctypes.byref(m), 0, 64, 4, 255, None, None, None, None, None) == 1
+    sl = _native.Slices()
+    assert L.dacsr_slices_fill(ctypes.byref(m), ctypes.byref(sl), None, None, None) == 1
+    assert L.dacsr_slices_medium_fill(ctypes.byref(m), ctypes.byref(sl), None) == 1
+    # a SLICED launch without a plan / without slices is a plan error
+    p = _native.Plan()
+    x = ctypes.c_void_p(8)
+    m.colids, m.values = 32, 64
+    assert L.dacsr_spmv(ctypes.byref(m), None, _native.VARIANT_CODES["sliced"], 0, x, 0, x,
+                        1.0, 0.0, 0, 64, None) == 5
+    assert L.dacsr_spmv(ctypes.byref(m), ctypes.byref(p), _native.VARIANT_CODES["sliced"], 0, x,
+                        0, x, 1.0, 0.0, 0, 64, None) == 5
