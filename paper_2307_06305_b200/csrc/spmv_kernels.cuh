@@ -752,6 +752,26 @@ __device__ __forceinline__ const VT* elem_addr(const VT* base, int64_t off) {
 #ifndef DACSR_SLICED_BATCH
 #define DACSR_SLICED_BATCH 8
 #endif
+// 16-bit values (and f32 with _F32) may trade batch size for occupancy
+#ifndef DACSR_SLICED_MINB_16
+#define DACSR_SLICED_MINB_16 DACSR_SLICED_MINB
+#endif
+#ifndef DACSR_SLICED_BATCH_16
+#define DACSR_SLICED_BATCH_16 DACSR_SLICED_BATCH
+#endif
+#ifndef DACSR_SLICED_MINB_32
+#define DACSR_SLICED_MINB_32 DACSR_SLICED_MINB
+#endif
+#ifndef DACSR_SLICED_BATCH_32
+#define DACSR_SLICED_BATCH_32 DACSR_SLICED_BATCH
+#endif
+template <class VT>
+struct SlicedTune {
+  static constexpr int minb = sizeof(VT) == 2 ? DACSR_SLICED_MINB_16
+                              : sizeof(VT) == 4 ? DACSR_SLICED_MINB_32 : DACSR_SLICED_MINB;
+  static constexpr int batch = sizeof(VT) == 2 ? DACSR_SLICED_BATCH_16
+                               : sizeof(VT) == 4 ? DACSR_SLICED_BATCH_32 : DACSR_SLICED_BATCH;
+};
 #ifndef DACSR_SLICED_PREFETCH
 #define DACSR_SLICED_PREFETCH 1
 #endif
@@ -823,10 +843,10 @@ struct SliceStage {
 // mbarrier, issued by lane 0), so only the x gathers sit in registers;
 // slices wider than wcap are read from HBM as in TMA == 0.
 template <int KIND, class RP, class CI, class VT, int TMA>
-__global__ void __launch_bounds__(256, DACSR_SLICED_MINB)
+__global__ void __launch_bounds__(256, SlicedTune<VT>::minb)
     sliced_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs, int64_t re,
                   int side_ctas, int wcap) {
-  constexpr int B = DACSR_SLICED_BATCH;
+  constexpr int B = SlicedTune<VT>::batch;
   using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
   using SS = SliceStage<CI, VT>;
   extern __shared__ __align__(128) unsigned char dsm[];

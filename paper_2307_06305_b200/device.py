@@ -341,6 +341,12 @@ class DeviceMatrix:
             times[k] = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
                                    min_epoch_time=0.0, cold=cold, graph=0 if cold else reps)
         self.tuned_kernel = min(times, key=times.get)
+        if self.tuned_kernel not in ("sliced", "sliced_tma") and self._sliced is not None:
+            # the sliced copy of the entries was only built to be timed
+            self._sliced = None
+            self._launch_cache.clear()
+            if getattr(self, "_streamed", None) is not None:
+                self._streamed._plans.clear()
         return times
 
     def set_ctas_per_sm(self, n):
