@@ -58,6 +58,14 @@ def test_c3_full_size(cuda):
     yd = dg.spmv(da, x, variant="naive")
     yc = dg.spmv(csr, x, variant="naive")
     assert torch.equal(yd, yc)  # naive CSR == naive DA bit-exact (reference crit 4)
+    # every exact kernel (both layouts) gives the same bits at full size
+    for dm in (da, csr):
+        for kernel in ("sliced", "sliced_tma", "wstream", "scalar"):
+            yk = torch.empty(n, dtype=torch.float64, device=cuda)
+            dm.spmv_into(x, yk, 1.0, 0.0, kernel, 0)
+            assert torch.equal(yk, yd), (dm.kind, kernel)
+        dm._sliced = None
+        dm._launch_cache.clear()
     # sampled rows against the oracle kernel on the copied row data
     xh = x.cpu().numpy()
     yh = yd.cpu().numpy()
@@ -93,7 +101,8 @@ def test_c4_rcm_and_skew(cuda):
     assert info["bandwidth_rcm"] == g["bandwidth_rcm"]
     d = dg.to_dacsr(a, 16)
     x = np.random.default_rng(3).uniform(-1, 1, a.ncols)
-    for variant in ("naive", "strip_mined_4"):
+    for variant in ("naive", "strip_mined_4", "sliced", "sliced_tma"):
         y = dg.spmv(d, x, variant=variant)
-        ref = oracle.spmv("da", d.rowptr, d.colids, d.values, x, order=variant, threads=8)
+        order = variant if variant in ("naive", "strip_mined_4") else "naive"
+        ref = oracle.spmv("da", d.rowptr, d.colids, d.values, x, order=order, threads=8)
         assert np.array_equal(y.view(np.uint64), ref.view(np.uint64)), variant
