@@ -463,8 +463,21 @@ def run_ours(args):
     if not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         t_cpu, var = cpu_measure("da", da, xh, threads)
+        # thread scaling of the same CPU path (T = 1, 2, 4, 8, all)
+        import oracle
+        y_cpu = np.empty(da.nrows)
+        scaling = {}
+        for t in sorted({1, 2, 4, 8, threads}):
+            if t > threads:
+                continue
+            fn = lambda t=t: oracle.spmv_kernel("da", da.rowptr, da.colids, da.values, xh, y_cpu,
+                                                1.0, 0.0, order=var, threads=t)
+            tt = oracle.time_kernel(fn, epochs=2, warmup_iters=1, min_epoch_iters=2,
+                                    min_epoch_time=0.05)
+            scaling[str(t)] = round(t_da / tt / 1e9, 2)
         line["cpu_baseline"] = {
             "value": round(t_da / t_cpu / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "gbs_by_threads": scaling,
             "kind": "port",
             "sample": f"C2 DA-CSR f64, one SpMV per iteration, best of the reference inner "
                       f"variants ('{var}' won) under ParallelRowBlock({threads}), 3 epochs of "
