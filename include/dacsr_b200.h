@@ -72,8 +72,11 @@ enum {
   DACSR_VARIANT_SLICED = 10,  /* sliced layout (plan->slices): lane per row,     */
                               /* coalesced column-major entries straight from    */
                               /* HBM, exact naive order; spill rows by side warps*/
-  DACSR_VARIANT_SLICED_TMA = 11 /* sliced layout, each warp's next two slices    */
+  DACSR_VARIANT_SLICED_TMA = 11, /* sliced layout, each warp's next two slices   */
                               /* staged in smem by TMA bulk copies              */
+  DACSR_VARIANT_SLICED_RING = 12 /* sliced layout, a producer warp streams       */
+                              /* multi-slice chunks into an smem ring for 8     */
+                              /* consumer warps (needs the padding below)       */
 };
 
 /* A matrix in CSR (absolute colids) or DA-CSR (colids = col - row) layout.
@@ -117,8 +120,9 @@ typedef struct {
   int64_t total;            /* main slots = slice_ptr[nslices]               */
   int32_t max_len;          /* main-slice rows: len <= max_len               */
   int32_t medium_len;       /* medium rows: max_len < len <= medium_len      */
-  const int64_t* slice_ptr; /* nslices + 1                                   */
-  const uint8_t* row_len;   /* row_end - row_start                           */
+  const int64_t* slice_ptr; /* nslices + 1 (SLICED_RING reads nslices + 2)   */
+  const uint8_t* row_len;   /* row_end - row_start (SLICED_RING reads 32 *   */
+                            /* nslices bytes: pad the buffer)                */
   const void* inner;        /* total, the matrix's colids dtype              */
   const void* values;       /* total, the matrix's values dtype              */
   int64_t n_medium;

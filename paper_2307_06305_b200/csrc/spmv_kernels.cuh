@@ -834,6 +834,38 @@ struct SliceStage {
   __host__ __device__ static constexpr int warp_bytes(int wcap) { return kStages * slot_bytes(wcap); }
 };
 
+// Medium slices t = first, first + stride, ... (32 listed rows each; lanes
+// whose row is outside [rs, re) skip), straight from HBM.  Call after
+// griddepcontrol.wait.
+template <int B, class OT, int KIND, class RP, class CI, class VT>
+__device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, const Scal& s,
+                                              const SliceArgs<CI, VT>& sl, int64_t rs,
+                                              int64_t re, int64_t first, int64_t stride,
+                                              int lane) {
+  const VT* __restrict__ xb = m.x + m.xoff;
+  for (int64_t t = first; t < sl.m_nslices; t += stride) {
+    const int64_t p0 = ldg(sl.mptr + t);
+    const int width = static_cast<int>((ldg(sl.mptr + t + 1) - p0) >> 5);
+    const int64_t k = 32 * t + lane;
+    int64_t r = -1;
+    int n = -1;
+    if (k < sl.n_medium) {
+      r = ldg(sl.mrows + k);
+      if (r >= rs && r < re) n = ldg(sl.len + (r - sl.row0));
+    }
+    const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
+    asm("" : "+l"(xr));
+    DACSR_CHECK(n <= width && width <= 254);
+    DACSR_CHECK(n <= 0 || p0 + lane + 32 * (n - 1) < sl.m_total);
+    const CI* pi = sl.mci + p0 + lane;
+    const VT* pv = sl.mv + p0 + lane;
+    const double acc = slice_row_dot<B, OT>(m, r, width, n, xr,
+                                            [&](int j) { return ldcs(pi + 32 * j); },
+                                            [&](int j) { return ldcs(pv + 32 * j); });
+    if (n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+  }
+}
+
 // SLICED kernel.  Each warp first takes its share of the medium slices
 // (rows outside [rs, re) skipped lane by lane), then its main slices of
 // [rs, re); long rows go to the first side_ctas CTAs.  TMA == 0: every slice straight from HBM with
@@ -868,30 +900,10 @@ __global__ void __launch_bounds__(256, SlicedTune<VT>::minb)
   bool waited = false;
 
   // medium slices (few, up to medium_len wide): straight from HBM
-  for (int64_t t = gw; t < sl.m_nslices; t += W) {
-    const int64_t p0 = ldg(sl.mptr + t);
-    const int width = static_cast<int>((ldg(sl.mptr + t + 1) - p0) >> 5);
-    const int64_t k = 32 * t + lane;
-    int64_t r = -1;
-    int n = -1;
-    if (k < sl.n_medium) {
-      r = ldg(sl.mrows + k);
-      if (r >= rs && r < re) n = ldg(sl.len + (r - sl.row0));
-    }
-    if (!waited) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      waited = true;
-    }
-    const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
-    asm("" : "+l"(xr));
-    DACSR_CHECK(n <= width && width <= 254);
-    DACSR_CHECK(n <= 0 || p0 + lane + 32 * (n - 1) < sl.m_total);
-    const CI* pi = sl.mci + p0 + lane;
-    const VT* pv = sl.mv + p0 + lane;
-    const double acc = slice_row_dot<B, OT>(m, r, width, n, xr,
-                                            [&](int j) { return ldcs(pi + 32 * j); },
-                                            [&](int j) { return ldcs(pv + 32 * j); });
-    if (n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+  if (gw < sl.m_nslices) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    waited = true;
+    medium_slices<B, OT>(m, s, sl, rs, re, gw, W, lane);
   }
 
   // main slices of [rs, re)
@@ -993,6 +1005,139 @@ __global__ void __launch_bounds__(256, SlicedTune<VT>::minb)
     stage(nxt2, slot);
     cur = nxt;
     nxt = nxt2;
+  }
+}
+
+// ------------------------------------------- SLICED_RING (warp-specialised)
+// One producer warp per CTA streams chunks of K consecutive main slices —
+// their values, inner indices, slice_ptr entries and row-length bytes, four
+// bulk copies per chunk — into an nstages-deep shared-memory ring (full /
+// empty mbarriers); the consumer warps take the chunk's slices round robin
+// and fold them from shared memory (lane l reads slot 32j + l: no bank
+// conflicts), gathering x from L2.  Large copies keep the DRAM stream dense
+// and no entry bytes occupy registers in flight.  The first side_ctas CTAs
+// take the medium slices and the long rows.
+// 16 consumer warps, 3 stages of <= 36 KiB, 2 CTAs/SM (measured best of
+// 8/16 consumers x 2/3/4 stages on C2 / C2-f32 / C2-bf16 / C4)
+#ifndef DACSR_RING_CONSUMERS
+#define DACSR_RING_CONSUMERS 16
+#endif
+constexpr int kRingMaxStages = 8;
+constexpr int kRingConsumers = DACSR_RING_CONSUMERS;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+template <class CI, class VT>
+struct RingStage {
+  // [values: vcap][inner: vcap, 16B-rounded][slice_ptr: K + 2][row_len: 32 K]
+  __host__ __device__ static constexpr int inner_off(int vcap) {
+    return (vcap * static_cast<int>(sizeof(VT)) + 15) & ~15;
+  }
+  __host__ __device__ static constexpr int ptr_off(int vcap) {
+    return inner_off(vcap) + ((vcap * static_cast<int>(sizeof(CI)) + 15) & ~15);
+  }
+  __host__ __device__ static constexpr int len_off(int vcap, int K) {
+    return ptr_off(vcap) + ((K + 2) * 8 + 15) / 16 * 16;
+  }
+  __host__ __device__ static constexpr int bytes(int vcap, int K) {
+    return len_off(vcap, K) + 32 * K;
+  }
+};
+
+template <int KIND, class RP, class CI, class VT>
+__global__ void __launch_bounds__(32 * (kRingConsumers + 1), 2)
+    sliced_ring_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs,
+                       int64_t re, int side_ctas, int K, int vcap, int nstages) {
+  constexpr int B = SlicedTune<VT>::batch;
+  using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
+  using RS = RingStage<CI, VT>;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (static_cast<int>(blockIdx.x) < side_ctas) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int nw = blockDim.x >> 5;
+    medium_slices<B, OT>(m, s, sl, rs, re, static_cast<int64_t>(blockIdx.x) * nw + warp,
+                         static_cast<int64_t>(side_ctas) * nw, lane);
+    long_rows(m, s, rs, re, sl.lrows, sl.n_long, blockIdx.x, side_ctas,
+              reinterpret_cast<double*>(dsm));
+    return;
+  }
+  __shared__ __align__(8) uint64_t full[kRingMaxStages], empty[kRingMaxStages];
+  const int64_t s0 = (rs - sl.row0) >> 5, s1 = (re - sl.row0 + 31) >> 5;
+  const int64_t nchunks = (s1 - s0 + K - 1) / K;
+  const int cta = blockIdx.x - side_ctas, ncta = gridDim.x - side_ctas;
+  const int sbytes = RS::bytes(vcap, K);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kRingConsumers);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kRingConsumers) {  // producer
+    if (lane == 0) {
+      int i = 0;
+      for (int64_t k = cta; k < nchunks; k += ncta, ++i) {
+        const int st = i % nstages;
+        if (i >= nstages) mbar_wait(&empty[st], static_cast<uint32_t>((i / nstages - 1) & 1));
+        const int64_t c0 = s0 + k * K, c1 = min64(c0 + K, s1);
+        const int64_t p0 = ldg(sl.ptr + c0), p1 = ldg(sl.ptr + c1);
+        const uint32_t slots = static_cast<uint32_t>(p1 - p0);
+        const int64_t ps = c0 & ~int64_t(1);                 // 16-byte aligned start
+        const uint32_t pn = static_cast<uint32_t>(((c1 + 1 - ps) + 1) & ~int64_t(1));
+        const uint32_t vb = slots * static_cast<uint32_t>(sizeof(VT));
+        const uint32_t ib = (slots * static_cast<uint32_t>(sizeof(CI)) + 15) & ~15u;
+        const uint32_t lb = static_cast<uint32_t>(32 * (c1 - c0));
+        unsigned char* dst = dsm + st * sbytes;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[st], (vb > 0 ? vb + ib : 0) + pn * 8 + lb);
+        if (vb > 0) {
+          bulk_copy_g2s(dst, sl.v + p0, vb, &full[st]);
+          bulk_copy_g2s(dst + RS::inner_off(vcap), sl.ci + p0, ib, &full[st]);
+        }
+        bulk_copy_g2s(dst + RS::ptr_off(vcap), sl.ptr + ps, pn * 8, &full[st]);
+        bulk_copy_g2s(dst + RS::len_off(vcap, K), sl.len + 32 * c0, lb, &full[st]);
+      }
+    }
+    return;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y from here on
+  const VT* __restrict__ xb = m.x + m.xoff;
+  int i = 0;
+  for (int64_t k = cta; k < nchunks; k += ncta, ++i) {
+    const int st = i % nstages;
+    mbar_wait(&full[st], static_cast<uint32_t>((i / nstages) & 1));
+    const unsigned char* base = dsm + st * sbytes;
+    const int64_t c0 = s0 + k * K, c1 = min64(c0 + K, s1);
+    const int64_t* sp = reinterpret_cast<const int64_t*>(base + RS::ptr_off(vcap)) + (c0 & 1);
+    const uint8_t* ln = base + RS::len_off(vcap, K);
+    const int64_t pc = sp[0];
+    for (int q = warp; q < c1 - c0; q += kRingConsumers) {
+      const int64_t c = c0 + q;
+      const int64_t p0 = sp[q];
+      const int width = static_cast<int>((sp[q + 1] - p0) >> 5);
+      const int64_t r = sl.row0 + 32 * c + lane;
+      int n = -1;
+      if (r >= rs && r < re) {
+        const int l = ln[32 * q + lane];
+        n = l > sl.max_len ? -1 : l;
+      }
+      const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
+      asm("" : "+l"(xr));
+      DACSR_CHECK(n <= width && width <= 254 && p0 - pc + 32 * width <= vcap);
+      const VT* pv = reinterpret_cast<const VT*>(base) + (p0 - pc) + lane;
+      const CI* pi = reinterpret_cast<const CI*>(base + RS::inner_off(vcap)) + (p0 - pc) + lane;
+      const double acc = slice_row_dot<B, OT>(m, r, width, n, xr,
+                                              [&](int j) { return pi[32 * j]; },
+                                              [&](int j) { return pv[32 * j]; });
+      if (n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
 }
 
@@ -1111,6 +1256,61 @@ int rowblock_stages(int cap) {
   const size_t budget = 100 * 1024;
   int st = static_cast<int>(budget / stage);
   return std::max(2, std::min(kMaxStages, st));
+}
+
+#ifndef DACSR_RING_STAGE_BYTES
+#define DACSR_RING_STAGE_BYTES (36 * 1024)
+#endif
+#ifndef DACSR_RING_STAGES
+#define DACSR_RING_STAGES 3
+#endif
+template <int KIND, class RP, class CI, class VT>
+int launch_ring(const Mat<KIND, RP, CI, VT>& m, const Scal& s, const SliceArgs<CI, VT>& sa,
+                const dacsr_slices_t* sd, const dacsr_plan_t* p, const Req& q, int sms) {
+  using RS = RingStage<CI, VT>;
+  // K slices per chunk: a multiple of the 8 consumer warps when a stage of
+  // that size fits the budget, else as many as fit (at least one)
+  const int per_slice = 32 * std::max(1, static_cast<int>(sd->max_len)) *
+                        static_cast<int>(sizeof(VT) + sizeof(CI));
+  int K = DACSR_RING_STAGE_BYTES / (per_slice + 40);
+  if (K >= kRingConsumers) K -= K % kRingConsumers;
+  K = std::max(1, std::min(K, 64));
+  const int vcap = 32 * K * std::max(1, static_cast<int>(sd->max_len));
+  int nstages = DACSR_RING_STAGES;
+  while (nstages > 2 && static_cast<size_t>(nstages) * RS::bytes(vcap, K) > 200 * 1024) --nstages;
+  const size_t ring_bytes = static_cast<size_t>(nstages) * RS::bytes(vcap, K);
+  const int threads = 32 * (kRingConsumers + 1);
+  const size_t side_bytes = sd->n_long > 0 ? static_cast<size_t>(threads / 32) * 128 * 8 : 0;
+  const size_t smem = std::max(ring_bytes, side_bytes);
+  auto kern = sliced_ring_kernel<KIND, RP, CI, VT>;
+  int per_sm = cached_per_sm(kern, threads, smem);
+  if (per_sm < 0) return check_launch("sliced_ring launch config");
+  if (p->ctas_per_sm > 0) per_sm = std::min(per_sm, static_cast<int>(p->ctas_per_sm));
+  const int64_t slots = static_cast<int64_t>(sms) * per_sm;
+  const int64_t nsl = ((q.re - sd->row_start + 31) >> 5) - ((q.rs - sd->row_start) >> 5);
+  const int64_t nchunks = (nsl + K - 1) / K;
+  const int64_t side_work = sd->m_nslices + sd->n_long;
+  const int side = side_work > 0 ? static_cast<int>(std::min<int64_t>(
+                                       (side_work + 2 * kRingConsumers - 1) / (2 * kRingConsumers),
+                                       std::max<int64_t>(1, slots / 8)))
+                                 : 0;
+  const int64_t grid = std::min<int64_t>(nchunks, std::max<int64_t>(slots - side, slots / 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(grid, 1) + side));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = q.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, sa, q.rs, q.re, side, K, vcap, nstages);
+  if (e != cudaSuccess) {
+    set_last_error("sliced_ring_kernel launch", e);
+    return DACSR_ERR_CUDA;
+  }
+  return check_launch("sliced_ring_kernel");
 }
 
 template <int KIND, class RP, class CI, class VT>
@@ -1245,7 +1445,8 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       return check_launch("wstream_kernel");
     }
     case DACSR_VARIANT_SLICED:
-    case DACSR_VARIANT_SLICED_TMA: {
+    case DACSR_VARIANT_SLICED_TMA:
+    case DACSR_VARIANT_SLICED_RING: {
       const dacsr_plan_t* p = q.plan;
       if (!p || !p->slices) return DACSR_ERR_PLAN;
       const dacsr_slices_t* sd = p->slices;
@@ -1270,6 +1471,8 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
                            sd->max_len, sd->medium_rows, sd->m_slice_ptr,
                            static_cast<const CI*>(sd->m_inner), static_cast<const VT*>(sd->m_values),
                            sd->n_medium, sd->m_nslices, sd->m_total, sd->long_rows, sd->n_long};
+      if (q.variant == DACSR_VARIANT_SLICED_RING)
+        return launch_ring<KIND, RP, CI, VT>(m, s, sa, sd, p, q, sms);
       constexpr int warps = 8, threads = 32 * warps;
       using SS = SliceStage<CI, VT>;
       const bool tma = q.variant == DACSR_VARIANT_SLICED_TMA && can_bulk_sl(sd);

@@ -265,17 +265,18 @@ class DeviceMatrix:
         dev = self.device
         sp = _stream_ptr(stream)
         vp = lambda t: ctypes.c_void_p(t.data_ptr())
-        row_len = torch.empty(max(re - rs, 1), dtype=torch.uint8, device=dev)
+        # padded for SLICED_RING's bulk copies: 32 bytes per slice, slice_ptr + 1
+        row_len = torch.zeros(max(32 * ns, 1), dtype=torch.uint8, device=dev)
         counts = torch.zeros(3, max(ns, 1), dtype=torch.int32, device=dev)
-        ptrs = torch.zeros(3, ns + 1, dtype=torch.int64, device=dev)
+        ptrs = torch.zeros(3, ns + 2, dtype=torch.int64, device=dev)
         with torch.cuda.device(dev):
             _native.check(L.dacsr_slices_count(
                 ctypes.byref(self.desc), rs, re, max_len, medium_len, vp(row_len), vp(counts[0]),
                 vp(counts[1]), vp(counts[2]), sp), "dacsr_slices_count")
             if ns:
                 for k in range(3):
-                    self._scan(counts[k, :ns], ptrs[k], sp)
-            total, n_medium, n_long = (int(v) for v in ptrs[:, -1].tolist())
+                    self._scan(counts[k, :ns], ptrs[k, :ns + 1], sp)
+            total, n_medium, n_long = (int(v) for v in ptrs[:, ns].tolist())
             inner = torch.empty(max(total, 1), dtype=self.colids.dtype, device=dev)
             values = torch.empty(max(total, 1), dtype=self.values.dtype, device=dev)
             medium_rows = torch.empty(max(n_medium, 1), dtype=torch.int64, device=dev)
@@ -323,8 +324,8 @@ class DeviceMatrix:
                 "bytes": sum(t.numel() * t.element_size() for t in tensors.values()
                              if t is not None)}
 
-    def autotune(self, candidates=("sliced", "sliced_tma", "wstream", "scalar", "rowblock",
-                                   "staged"), cold=False,
+    def autotune(self, candidates=("sliced", "sliced_ring", "sliced_tma", "wstream", "scalar",
+                                   "rowblock", "staged"), cold=False,
                  x=None, reps=5):
         """Time the exact naive-order kernels on this matrix and remember the
         fastest for variant "naive"/"auto" (all give bit-identical results,
@@ -335,13 +336,14 @@ class DeviceMatrix:
         y = torch.empty(self.nrows, dtype=self.values.dtype, device=self.device)
         times = {}
         for k in candidates:
-            if k in ("wstream", "rowblock", "sliced", "sliced_tma") and self.plan is None:
+            if k in ("wstream", "rowblock", "sliced", "sliced_tma", "sliced_ring") and self.plan is None:
                 continue
             fn = lambda k=k: self.spmv_into(x, y, 1.0, 0.0, k, 0)
             times[k] = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
                                    min_epoch_time=0.0, cold=cold, graph=0 if cold else reps)
         self.tuned_kernel = min(times, key=times.get)
-        if self.tuned_kernel not in ("sliced", "sliced_tma") and self._sliced is not None:
+        if (self.tuned_kernel not in ("sliced", "sliced_tma", "sliced_ring")
+                and self._sliced is not None):
             # the sliced copy of the entries was only built to be timed
             self._sliced = None
             self._launch_cache.clear()
@@ -371,7 +373,7 @@ class DeviceMatrix:
         differs from the planned one)."""
         rs = self.row_start if row_start is None else row_start
         re = self.row_end if row_end is None else row_end
-        if kname in ("sliced", "sliced_tma"):  # the slices serve any row range inside theirs
+        if kname in ("sliced", "sliced_tma", "sliced_ring"):  # any row range inside theirs
             if not (self.row_start <= rs <= re <= self.row_end):
                 return None
             return self._sliced[0] if self._sliced is not None else self.build_slices()
