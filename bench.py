@@ -68,12 +68,14 @@ def peaks():
 
 
 def ncu_traffic(kernel_key):
-    """(dram bytes per launch, note) from the committed ncu summary, if present."""
+    """(dram bytes per cold launch from the ncu --set full capture, the
+    steady-state record inside the bench step) from the committed ncu
+    summary, if present."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             rec = json.load(f).get(kernel_key, {})
-        return rec.get("dram_bytes_per_launch"), rec.get("note")
+        return rec.get("dram_bytes_per_launch"), rec.get("steady_state_in_step")
     except (OSError, ValueError):
         return None, None
 
@@ -423,7 +425,8 @@ def run_ours(args):
     peak, peak_src = peaks()
     per_launch = step_s / SPMV_PER_STEP
     achieved = t_da / per_launch / 1e9
-    traffic, traffic_note = ncu_traffic(kname + ":c2:da")
+    traffic, steady = ncu_traffic(kname + ":c2:da")
+    steady_bytes = steady.get("dram_bytes_per_launch") if steady else None
     line = {
         "metric": "SpMV effective HBM GB/s (DA-CSR i16, f64)",
         "value": round(value, 1), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
@@ -438,11 +441,13 @@ def run_ours(args):
                    "parallelism": "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "traffic_note": traffic_note,
-                     "dram_gbs_at_traffic": (round(traffic / per_launch / 1e9, 1)
-                                             if traffic else None),
-                     "dram_frac_at_traffic": (round(traffic / per_launch / 1e9 / peak, 4)
-                                              if traffic else None),
+                     "traffic_source": "ncu --set full, one cold launch (profiles/)",
+                     "traffic_steady_state": steady_bytes,
+                     "traffic_steady_state_note": steady.get("note") if steady else None,
+                     "dram_gbs_steady_state": (round(steady_bytes / per_launch / 1e9, 1)
+                                               if steady_bytes else None),
+                     "dram_frac_steady_state": (round(steady_bytes / per_launch / 1e9 / peak, 4)
+                                                if steady_bytes else None),
                      "peak_source": peak_src, "bytes_per_launch": t_da,
                      "frac_of_nominal_8TBs": round(achieved / 8000.0, 4),
                      "frac_of_tma_read_ceiling": round(achieved / READ_CEILING_GBS, 4),
