@@ -74,9 +74,12 @@ enum {
                               /* HBM, exact naive order; spill rows by side warps*/
   DACSR_VARIANT_SLICED_TMA = 11, /* sliced layout, each warp's next two slices   */
                               /* staged in smem by TMA bulk copies              */
-  DACSR_VARIANT_SLICED_RING = 12 /* sliced layout, a producer warp streams       */
-                              /* multi-slice chunks into an smem ring for 8     */
+  DACSR_VARIANT_SLICED_RING = 12, /* sliced layout, a producer warp streams      */
+                              /* multi-slice chunks into an smem ring for the   */
                               /* consumer warps (needs the padding below)       */
+  DACSR_VARIANT_SLICED_PRED = 13 /* SLICED + x gathers issued at the offsets of  */
+                              /* the warp's previous slice (stencil-like rows), */
+                              /* re-gathered when the guess was wrong          */
 };
 
 /* A matrix in CSR (absolute colids) or DA-CSR (colids = col - row) layout.

@@ -820,6 +820,43 @@ __device__ __forceinline__ double slice_row_dot(const Mat<KIND, RP, CI, VT>& m, 
   return acc;
 }
 
+// First batch of a lane's row with offset prediction (SLICED_PRED): the x
+// gathers are issued at the offsets this lane saw in the warp's previous
+// slice — for stencil-like matrices the same, since a warp's slices are W
+// slices apart — together with the entry loads, so a correct guess removes
+// the entries -> gathers round trip.  Wrong guesses (compared after the
+// offsets arrive) are gathered again; guesses are clamped into x so the
+// speculative loads stay in bounds.  pred[] is updated to this slice's
+// offsets.  Results are identical whatever the guesses.
+template <int B, class OT, int KIND, class RP, class CI, class VT, class LI, class LV>
+__device__ __forceinline__ double slice_row_dot_pred(const Mat<KIND, RP, CI, VT>& m, int64_t r,
+                                                     int width, int n, const VT* xr,
+                                                     const LI& li, const LV& lv, OT* pred,
+                                                     OT omin, OT omax) {
+  OT o[B];
+  VT vv[B], xs[B];
+#pragma unroll
+  for (int u = 0; u < B; ++u) {
+    const bool on = u < n;
+    const OT g = pred[u] < omin ? omin : (pred[u] > omax ? omax : pred[u]);
+    xs[u] = on ? ldg(elem_addr(xr, g)) : VT(0);
+    o[u] = on ? static_cast<OT>(li(u)) : OT(0);
+    vv[u] = on ? lv(u) : VT(0);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < B; ++u) {
+    const bool on = u < n;
+    if (on) m.check(r, 0, static_cast<CI>(o[u]));
+    const VT xv = !on ? VT(0) : (o[u] == pred[u] ? xs[u] : ldg(elem_addr(xr, o[u])));
+    if (on) pred[u] = o[u];
+    acc = __dadd_rn(acc, product(vv[u], xv));
+  }
+  if (width > B)
+    acc = slice_row_dot<B, OT>(m, r, width, n, xr, li, lv, B, acc);
+  return acc;
+}
+
 // Per-warp staging of the sliced layout: kStages slots of one slice each
 // (values, then inner indices), slices up to `wcap` entries per lane.
 template <class CI, class VT>
@@ -874,8 +911,11 @@ __device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, co
 // two slices in flight in its shared-memory stages (cp.async.bulk +
 // mbarrier, issued by lane 0), so only the x gathers sit in registers;
 // slices wider than wcap are read from HBM as in TMA == 0.
+#ifndef DACSR_SLICED_PRED_MINB
+#define DACSR_SLICED_PRED_MINB 3
+#endif
 template <int KIND, class RP, class CI, class VT, int TMA>
-__global__ void __launch_bounds__(256, SlicedTune<VT>::minb)
+__global__ void __launch_bounds__(256, TMA == 3 ? DACSR_SLICED_PRED_MINB : SlicedTune<VT>::minb)
     sliced_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs, int64_t re,
                   int side_ctas, int wcap) {
   constexpr int B = SlicedTune<VT>::batch;
@@ -967,6 +1007,9 @@ __global__ void __launch_bounds__(256, SlicedTune<VT>::minb)
   stage(nxt, 1);
   if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
   uint32_t phase = 0;
+  OT pred[B];
+#pragma unroll
+  for (int u = 0; u < B; ++u) pred[u] = OT(0);
   for (int k = 0; c < s1; c += W, ++k) {
     const int slot = k & 1;
     const Raw raw2 = load_raw(c + 2 * W);
@@ -987,6 +1030,16 @@ __global__ void __launch_bounds__(256, SlicedTune<VT>::minb)
       acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
                                  [&](int j) { return pi[32 * j]; },
                                  [&](int j) { return pv[32 * j]; });
+    } else if (TMA == 3) {
+      const CI* pi = sl.ci + cur.p0 + lane;
+      const VT* pv = sl.v + cur.p0 + lane;
+      // valid guesses keep the column inside x (x_offset is 0 in this mode)
+      const OT omin = KIND == DACSR_KIND_DA ? static_cast<OT>(-r) : OT(0);
+      const OT omax = static_cast<OT>((KIND == DACSR_KIND_DA ? m.ncols - 1 - r : m.ncols - 1));
+      acc = slice_row_dot_pred<B, OT>(m, r, cur.width, cur.n, xr,
+                                      [&](int j) { return ldcs(pi + 32 * j); },
+                                      [&](int j) { return ldcs(pv + 32 * j); }, pred, omin,
+                                      omax);
     } else {
       const CI* pi = sl.ci + cur.p0 + lane;
       const VT* pv = sl.v + cur.p0 + lane;
@@ -1446,7 +1499,8 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
     }
     case DACSR_VARIANT_SLICED:
     case DACSR_VARIANT_SLICED_TMA:
-    case DACSR_VARIANT_SLICED_RING: {
+    case DACSR_VARIANT_SLICED_RING:
+    case DACSR_VARIANT_SLICED_PRED: {
       const dacsr_plan_t* p = q.plan;
       if (!p || !p->slices) return DACSR_ERR_PLAN;
       const dacsr_slices_t* sd = p->slices;
@@ -1486,7 +1540,10 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       const size_t stage_bytes = tma ? static_cast<size_t>(warps) * SS::warp_bytes(wcap) : 0;
       const size_t side_bytes = sd->n_long > 0 ? static_cast<size_t>(warps) * 128 * 8 : 0;
       const size_t smem = std::max(stage_bytes, side_bytes);
-      auto kern = tma ? sliced_kernel<KIND, RP, CI, VT, 1> : sliced_kernel<KIND, RP, CI, VT, 0>;
+      // prediction needs the true x extent (no rank-local x_offset)
+      const bool pred = q.variant == DACSR_VARIANT_SLICED_PRED && q.xoff == 0 && a->ncols > 0;
+      auto kern = tma ? sliced_kernel<KIND, RP, CI, VT, 1>
+                      : pred ? sliced_kernel<KIND, RP, CI, VT, 3> : sliced_kernel<KIND, RP, CI, VT, 0>;
       int per_sm = cached_per_sm(kern, threads, smem);
       if (per_sm < 0) return check_launch("sliced launch config");
       if (p->ctas_per_sm > 0) per_sm = std::min(per_sm, static_cast<int>(p->ctas_per_sm));

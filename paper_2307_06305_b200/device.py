@@ -27,6 +27,9 @@ import torch
 from . import _native
 from .core import CsrMatrix, DacsrMatrix
 
+# kernels that run on the sliced layout (DeviceMatrix.build_slices)
+SLICED_KERNELS = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred")
+
 _KIND_NAME = {_native.KIND_CSR: "csr", _native.KIND_DA: "da"}
 
 
@@ -324,8 +327,8 @@ class DeviceMatrix:
                 "bytes": sum(t.numel() * t.element_size() for t in tensors.values()
                              if t is not None)}
 
-    def autotune(self, candidates=("sliced", "sliced_ring", "sliced_tma", "wstream", "scalar",
-                                   "rowblock", "staged"), cold=False,
+    def autotune(self, candidates=("sliced", "sliced_pred", "sliced_ring", "sliced_tma",
+                                   "wstream", "scalar", "rowblock", "staged"), cold=False,
                  x=None, reps=5):
         """Time the exact naive-order kernels on this matrix and remember the
         fastest for variant "naive"/"auto" (all give bit-identical results,
@@ -336,14 +339,13 @@ class DeviceMatrix:
         y = torch.empty(self.nrows, dtype=self.values.dtype, device=self.device)
         times = {}
         for k in candidates:
-            if k in ("wstream", "rowblock", "sliced", "sliced_tma", "sliced_ring") and self.plan is None:
+            if (k in ("wstream", "rowblock") or k in SLICED_KERNELS) and self.plan is None:
                 continue
             fn = lambda k=k: self.spmv_into(x, y, 1.0, 0.0, k, 0)
             times[k] = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
                                    min_epoch_time=0.0, cold=cold, graph=0 if cold else reps)
         self.tuned_kernel = min(times, key=times.get)
-        if (self.tuned_kernel not in ("sliced", "sliced_tma", "sliced_ring")
-                and self._sliced is not None):
+        if self.tuned_kernel not in SLICED_KERNELS and self._sliced is not None:
             # the sliced copy of the entries was only built to be timed
             self._sliced = None
             self._launch_cache.clear()
@@ -373,7 +375,7 @@ class DeviceMatrix:
         differs from the planned one)."""
         rs = self.row_start if row_start is None else row_start
         re = self.row_end if row_end is None else row_end
-        if kname in ("sliced", "sliced_tma", "sliced_ring"):  # any row range inside theirs
+        if kname in SLICED_KERNELS:  # any row range inside theirs
             if not (self.row_start <= rs <= re <= self.row_end):
                 return None
             return self._sliced[0] if self._sliced is not None else self.build_slices()

@@ -163,7 +163,7 @@ class CudaLocalOp:
         name, order = resolve_variant(variant)
         self.order = order
         self.mats = []
-        if name in ("sliced", "sliced_tma", "sliced_ring") and n_local:
+        if name in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred") and n_local:
             # one sliced layout of all local rows serves the three row ranges
             full = DeviceMatrix(kind, n_local, ncols_global, rowptr, colids, values)
             full.build_slices()

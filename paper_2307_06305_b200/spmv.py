@@ -49,7 +49,8 @@ _EXACT = {
     "strip_mined_4": ("exact", _native.ORDER_STRIP4),
 }
 _EXACT_KERNELS = ("rowblock", "staged", "scalar", "wstream", "sliced", "sliced_tma",
-                  "sliced_ring")
+                  "sliced_ring", "sliced_pred")
+_SLICED = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred")  # the sliced layout
 _TREE_KERNELS = ("vector2", "vector4", "vector8", "vector16", "warp")
 GPU_VARIANTS = ("auto", "rowblock_tree") + _EXACT_KERNELS + _TREE_KERNELS
 _CODE_NAME = {v: k for k, v in _native.VARIANT_CODES.items()}
@@ -129,9 +130,9 @@ def kernel_for(dm, kname, order):
         if dm.stats is None:
             return "staged"
         kname = _CODE_NAME[_native.lib().dacsr_select_variant(dm.stats, order)]
-    if kname in ("wstream", "sliced", "sliced_tma", "sliced_ring") and order in (_native.ORDER_MACC3, _native.ORDER_STRIP4):
+    if kname in ("wstream",) + _SLICED and order in (_native.ORDER_MACC3, _native.ORDER_STRIP4):
         kname = "rowblock"  # warp streams / slices specialise the naive order
-    if kname in ("rowblock", "wstream", "sliced", "sliced_tma", "sliced_ring") and dm.plan is None:
+    if kname in ("rowblock", "wstream") + _SLICED and dm.plan is None:
         return "staged"
     return kname
 

@@ -65,6 +65,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--variant", default="sliced")
 ap.add_argument("--configs", default="c2,c2f32,c2bf16,c1,c4")
 ap.add_argument("--kinds", default="da")
+ap.add_argument("--no-check", action="store_true", help="timing-only builds (results not exact)")
 ap.add_argument("libs", nargs="+")
 args = ap.parse_args()
 for lib in args.libs:
