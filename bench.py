@@ -343,8 +343,12 @@ def run_c5(args, world, rank, local):
     o = dm.oindex_width // 8
     traffic = traffic_of(n, dm.nnz, o, 2, 8)
     iters = 50
+    # the fastest exact kernel on this operator (all give the same bits)
+    tuned = {k: round(v * 1e3, 3) for k, v in
+             dm.autotune(x=x0, reps=3, candidates=("sliced", "wstream", "rowblock", "scalar")).items()}
+    kname = dm.tuned_kernel
     for _ in range(args.warmup):
-        power_iteration(dm, x0, iters=2)
+        power_iteration(dm, x0, iters=2, variant=kname)
     torch.cuda.synchronize()
     times = []
     with ClockSampler(local) as clocks:
@@ -352,7 +356,7 @@ def run_c5(args, world, rank, local):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            _, norms = power_iteration(dm, x0, iters=iters)
+            _, norms = power_iteration(dm, x0, iters=iters, variant=kname)
             e1.record()
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
@@ -367,7 +371,9 @@ def run_c5(args, world, rank, local):
         "config": {"workload": "C5: power iteration, 50 iters, banded n=2^28 b=32767 "
                                "Poisson(8) in [1,32], DA-CSR i16 + int64 rowptr",
                    "nnz": dm.nnz, "bytes_per_spmv": traffic, "build_s": round(build_s, 1),
-                   "final_norm": norms[-1]},
+                   "final_norm": norms[-1], "kernel": kname,
+                   "kernel_selection": "fastest exact kernel, warm ms per SpMV: "
+                                       + json.dumps(tuned)},
         "roofline": {"bound": "hbm", "achieved": round(iters * traffic / step / 1e9, 1),
                      "peak": peak, "unit": "GB/s",
                      "frac": round(iters * traffic / step / 1e9 / peak, 4), "traffic": None,
