@@ -90,19 +90,26 @@ def time_kernel(fn, epochs=11, warmup_iters=10, min_epoch_iters=10, min_epoch_ti
                 elapsed += e0.elapsed_time(e1) / 1e3
                 iters += 1
         else:
+            # the epoch repeats fn until both min_epoch_iters and
+            # min_epoch_time of DEVICE time are covered; the count comes from
+            # the device time of one batch (a host-time loop would enqueue far
+            # more work than intended when one call is milliseconds long)
+            batch = max(1, min_epoch_iters)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            batch = max(1, min_epoch_iters)
             e0.record(stream)
-            t0 = time.perf_counter()
-            while True:
-                for _ in range(batch):
-                    fn()
-                iters += batch
-                if time.perf_counter() - t0 >= min_epoch_time or iters >= 1_000_000:
-                    break
+            for _ in range(batch):
+                fn()
             e1.record(stream)
             e1.synchronize()
+            t_batch = max(e0.elapsed_time(e1) / 1e3, 1e-9)
+            reps = max(1, min(1_000_000 // batch, math.ceil(min_epoch_time / t_batch)))
+            e0.record(stream)
+            for _ in range(reps * batch):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            iters = reps * batch
             elapsed = e0.elapsed_time(e1) / 1e3
         best = min(best, elapsed / (iters * per_call))
     return best
