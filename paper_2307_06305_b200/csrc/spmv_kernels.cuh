@@ -905,12 +905,16 @@ __device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, co
 
 // SLICED kernel.  Each warp first takes its share of the medium slices
 // (rows outside [rs, re) skipped lane by lane), then its main slices of
-// [rs, re); long rows go to the first side_ctas CTAs.  TMA == 0: every slice straight from HBM with
-// coalesced loads, the entries of the slice two steps ahead pulled into L2
-// by a bulk prefetch.  TMA == 1: each warp keeps the entries of its next
-// two slices in flight in its shared-memory stages (cp.async.bulk +
-// mbarrier, issued by lane 0), so only the x gathers sit in registers;
-// slices wider than wcap are read from HBM as in TMA == 0.
+// [rs, re); long rows go to the first side_ctas CTAs.  The mode (TMA):
+//  0  SLICED: every slice straight from HBM with coalesced loads; the
+//     entries of the slice two steps ahead are pulled into L2 by a bulk
+//     prefetch (slice metadata is loaded one step earlier still).
+//  1  SLICED_TMA: each warp keeps the entries of its next two slices in
+//     flight in its shared-memory stages (cp.async.bulk + mbarrier, issued
+//     by lane 0), so only the x gathers sit in registers; slices wider
+//     than wcap are read from HBM as in mode 0.
+//  3  SLICED_PRED: mode 0 with offset-predicted first-batch gathers
+//     (slice_row_dot_pred), 80 registers.
 #ifndef DACSR_SLICED_PRED_MINB
 #define DACSR_SLICED_PRED_MINB 3
 #endif
