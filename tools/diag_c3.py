@@ -1,3 +1,6 @@
+"""C3 (random band): per-kernel cold / warm time of every exact kernel, with
+progress timestamps (diagnosed the harness over-enqueue that made warm
+timings of millisecond SpMVs take minutes)."""
 import sys, time
 sys.path.insert(0, ".")
 import torch
