@@ -338,12 +338,36 @@ class DeviceMatrix:
             x = torch.ones(self.ncols, dtype=self.values.dtype, device=self.device)
         y = torch.empty(self.nrows, dtype=self.values.dtype, device=self.device)
         times = {}
+
+        def timed(k):
+            fn = lambda: self.spmv_into(x, y, 1.0, 0.0, k, 0)
+            return time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
+                               min_epoch_time=0.0, cold=cold, graph=0 if cold else reps)
+
+        if "sliced" in candidates and self.plan is not None and self.nnz:
+            # the main/medium split changes the slice widths a warp walks:
+            # time the cost model's choice against 8 and 16 (one batch or
+            # two per slice) and keep the fastest layout
+            model = self.slice_max_len()
+            longest = int(self.stats.max_len) if self.stats is not None else 254
+            tried = {}
+            for t in sorted({model, 8, 16}):
+                t = min(t, max(1, longest))
+                if t in tried:
+                    continue
+                self.build_slices(t)
+                tried[t] = timed("sliced")
+            best_t = min(tried, key=tried.get)
+            if self._sliced is None or self._sliced[1].max_len != best_t:
+                self.build_slices(best_t)
+            times["sliced"] = tried[best_t]
+            self.slice_max_len_tuned = {int(k): v for k, v in tried.items()}
         for k in candidates:
+            if k in times:
+                continue
             if (k in ("wstream", "rowblock") or k in SLICED_KERNELS) and self.plan is None:
                 continue
-            fn = lambda k=k: self.spmv_into(x, y, 1.0, 0.0, k, 0)
-            times[k] = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
-                                   min_epoch_time=0.0, cold=cold, graph=0 if cold else reps)
+            times[k] = timed(k)
         self.tuned_kernel = min(times, key=times.get)
         if self.tuned_kernel not in SLICED_KERNELS and self._sliced is not None:
             # the sliced copy of the entries was only built to be timed
