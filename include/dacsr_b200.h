@@ -77,9 +77,11 @@ enum {
   DACSR_VARIANT_SLICED_RING = 12, /* sliced layout, a producer warp streams      */
                               /* multi-slice chunks into an smem ring for the   */
                               /* consumer warps (needs the padding below)       */
-  DACSR_VARIANT_SLICED_PRED = 13 /* SLICED + x gathers issued at the offsets of  */
+  DACSR_VARIANT_SLICED_PRED = 13, /* SLICED + x gathers issued at the offsets of */
                               /* the warp's previous slice (stencil-like rows), */
                               /* re-gathered when the guess was wrong          */
+  DACSR_VARIANT_SLICED_PIPE = 14 /* SLICED with the next slice's offsets loaded  */
+                              /* while this slice's gathers are in flight       */
 };
 
 /* A matrix in CSR (absolute colids) or DA-CSR (colids = col - row) layout.

@@ -915,11 +915,21 @@ __device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, co
 //     than wcap are read from HBM as in mode 0.
 //  3  SLICED_PRED: mode 0 with offset-predicted first-batch gathers
 //     (slice_row_dot_pred), 80 registers.
+//  4  SLICED_PIPE: mode 0 with the next slice's first-batch offsets loaded
+//     while this slice's gathers and values are in flight (one memory round
+//     per slice instead of two), 80 registers.
 #ifndef DACSR_SLICED_PRED_MINB
 #define DACSR_SLICED_PRED_MINB 3
 #endif
+// SLICED_PIPE holds the next slice's offsets across the iteration: 80
+// registers, 3 CTAs/SM (measured: 64 registers spill and run 27 % slower)
+#ifndef DACSR_SLICED_PIPE_MINB
+#define DACSR_SLICED_PIPE_MINB 3
+#endif
 template <int KIND, class RP, class CI, class VT, int TMA>
-__global__ void __launch_bounds__(256, TMA == 3 ? DACSR_SLICED_PRED_MINB : SlicedTune<VT>::minb)
+__global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
+                                       : TMA == 4 ? DACSR_SLICED_PIPE_MINB
+                                                  : SlicedTune<VT>::minb)
     sliced_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs, int64_t re,
                   int side_ctas, int wcap) {
   constexpr int B = SlicedTune<VT>::batch;
@@ -1005,6 +1015,57 @@ __global__ void __launch_bounds__(256, TMA == 3 ? DACSR_SLICED_PRED_MINB : Slice
       prefetch_l2_bulk(sl.ci + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(CI)) & ~15u);
     }
   };
+  if constexpr (TMA == 4) {
+    // offsets one slice ahead: the first batch's offsets of the next slice
+    // are loaded while this slice's gathers and values are in flight, so
+    // each slice costs one memory round (gathers + values) instead of two
+    // (offsets, then gathers).  Only the offsets (not the values) are held
+    // across the iteration, which keeps the batch within 64 registers.
+    Meta cur = derive(load_raw(c));
+    Meta nxt = derive(load_raw(c + W));
+    stage(nxt, 1);
+    OT oc[B];
+    auto load_offsets = [&](const Meta& q, OT* o) {
+      const CI* pi = sl.ci + q.p0 + lane;
+#pragma unroll
+      for (int u = 0; u < B; ++u) o[u] = u < q.n ? static_cast<OT>(ldcs(pi + 32 * u)) : OT(0);
+    };
+    load_offsets(cur, oc);
+    if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (; c < s1; c += W) {
+      const Raw raw2 = load_raw(c + 2 * W);
+      const int64_t r = sl.row0 + 32 * c + lane;
+      const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
+      asm("" : "+l"(xr));
+      DACSR_CHECK(cur.n <= cur.width && cur.width <= 254);
+      DACSR_CHECK(cur.n <= 0 || cur.p0 + lane + 32 * (cur.n - 1) < sl.total);
+      const VT* pv = sl.v + cur.p0 + lane;
+      VT xv[B], vv[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const bool on = u < cur.n;
+        if (on) m.check(r, 0, static_cast<CI>(oc[u]));
+        xv[u] = on ? ldg(elem_addr(xr, oc[u])) : VT(0);
+        vv[u] = on ? ldcs(pv + 32 * u) : VT(0);
+      }
+      load_offsets(nxt, oc);
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, product(vv[u], xv[u]));
+      if (cur.width > B) {  // the rest of a wider slice: the plain loop
+        const CI* pi = sl.ci + cur.p0 + lane;
+        acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
+                                   [&](int j) { return ldcs(pi + 32 * j); },
+                                   [&](int j) { return ldcs(pv + 32 * j); }, B, acc);
+      }
+      if (cur.n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+      const Meta nxt2 = derive(raw2);
+      stage(nxt2, 0);
+      cur = nxt;
+      nxt = nxt2;
+    }
+    return;
+  }
   Meta cur = derive(load_raw(c));
   Meta nxt = derive(load_raw(c + W));
   if (TMA == 1) stage(cur, 0);
@@ -1504,7 +1565,8 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
     case DACSR_VARIANT_SLICED:
     case DACSR_VARIANT_SLICED_TMA:
     case DACSR_VARIANT_SLICED_RING:
-    case DACSR_VARIANT_SLICED_PRED: {
+    case DACSR_VARIANT_SLICED_PRED:
+    case DACSR_VARIANT_SLICED_PIPE: {
       const dacsr_plan_t* p = q.plan;
       if (!p || !p->slices) return DACSR_ERR_PLAN;
       const dacsr_slices_t* sd = p->slices;
@@ -1546,8 +1608,14 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       const size_t smem = std::max(stage_bytes, side_bytes);
       // prediction needs the true x extent (no rank-local x_offset)
       const bool pred = q.variant == DACSR_VARIANT_SLICED_PRED && q.xoff == 0 && a->ncols > 0;
-      auto kern = tma ? sliced_kernel<KIND, RP, CI, VT, 1>
-                      : pred ? sliced_kernel<KIND, RP, CI, VT, 3> : sliced_kernel<KIND, RP, CI, VT, 0>;
+#ifndef DACSR_SLICED_DEFAULT_MODE
+#define DACSR_SLICED_DEFAULT_MODE 0
+#endif
+      auto kern = tma    ? sliced_kernel<KIND, RP, CI, VT, 1>
+                  : pred ? sliced_kernel<KIND, RP, CI, VT, 3>
+                  : q.variant == DACSR_VARIANT_SLICED_PIPE
+                      ? sliced_kernel<KIND, RP, CI, VT, 4>
+                      : sliced_kernel<KIND, RP, CI, VT, DACSR_SLICED_DEFAULT_MODE>;
       int per_sm = cached_per_sm(kern, threads, smem);
       if (per_sm < 0) return check_launch("sliced launch config");
       if (p->ctas_per_sm > 0) per_sm = std::min(per_sm, static_cast<int>(p->ctas_per_sm));

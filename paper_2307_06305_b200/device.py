@@ -28,7 +28,7 @@ from . import _native
 from .core import CsrMatrix, DacsrMatrix
 
 # kernels that run on the sliced layout (DeviceMatrix.build_slices)
-SLICED_KERNELS = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred")
+SLICED_KERNELS = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe")
 
 _KIND_NAME = {_native.KIND_CSR: "csr", _native.KIND_DA: "da"}
 
@@ -327,8 +327,9 @@ class DeviceMatrix:
                 "bytes": sum(t.numel() * t.element_size() for t in tensors.values()
                              if t is not None)}
 
-    def autotune(self, candidates=("sliced", "sliced_pred", "sliced_ring", "sliced_tma",
-                                   "wstream", "scalar", "rowblock", "staged"), cold=False,
+    def autotune(self, candidates=("sliced", "sliced_pipe", "sliced_pred", "sliced_ring",
+                                   "sliced_tma", "wstream", "scalar", "rowblock", "staged"),
+                 cold=False,
                  x=None, reps=5):
         """Time the exact naive-order kernels on this matrix and remember the
         fastest for variant "naive"/"auto" (all give bit-identical results,

@@ -163,7 +163,7 @@ class CudaLocalOp:
         name, order = resolve_variant(variant)
         self.order = order
         self.mats = []
-        if name in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred") and n_local:
+        if name in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe") and n_local:
             # one sliced layout of all local rows serves the three row ranges
             full = DeviceMatrix(kind, n_local, ncols_global, rowptr, colids, values)
             full.build_slices()
@@ -324,7 +324,7 @@ def bench_main(args, rank, world, local):
     # capture on a multi-rank communicator is not worth the risk before the
     # timed run; at N > 1 the kernel measured fastest at one rank is used)
     tuned = {}
-    for cand in (("sliced", "wstream") if world == 1 else ("sliced",)):
+    for cand in (("sliced_pipe", "sliced", "wstream") if world == 1 else ("sliced_pipe",)):
         op = CudaLocalOp("da", t_rp, t_off, t_val, n, plan, 1 << 16, plane, variant=cand)
         def burst(op=op):
             for _ in range(20):

@@ -62,7 +62,7 @@ class StreamedHost:
         if rec is None:
             k = kernel_for(self.dm, kname, order)
             plans = (_native.Plan * len(self.views))()
-            if k in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred"):
+            if k in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"):
                 # the pieces share the whole matrix's sliced layout (the
                 # kernel takes any row range inside it); no row-block table
                 pl = self.dm.plan_for(k)

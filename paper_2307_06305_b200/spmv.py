@@ -49,8 +49,8 @@ _EXACT = {
     "strip_mined_4": ("exact", _native.ORDER_STRIP4),
 }
 _EXACT_KERNELS = ("rowblock", "staged", "scalar", "wstream", "sliced", "sliced_tma",
-                  "sliced_ring", "sliced_pred")
-_SLICED = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred")  # the sliced layout
+                  "sliced_ring", "sliced_pred", "sliced_pipe")
+_SLICED = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe")  # the sliced layout
 _TREE_KERNELS = ("vector2", "vector4", "vector8", "vector16", "warp")
 GPU_VARIANTS = ("auto", "rowblock_tree") + _EXACT_KERNELS + _TREE_KERNELS
 _CODE_NAME = {v: k for k, v in _native.VARIANT_CODES.items()}

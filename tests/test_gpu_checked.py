@@ -26,7 +26,7 @@ from paper_2307_06305_b200.workloads import add_skew_rows, laplacian_2d, uniform
 from test_oracle import CORPUS
 assert _native.LIB_PATH.endswith("_checked.so"), _native.LIB_PATH
 dev = torch.device("cuda")
-kernels = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "wstream", "rowblock", "staged", "scalar", "vector4", "warp", "rowblock_tree",
+kernels = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe", "wstream", "rowblock", "staged", "scalar", "vector4", "warp", "rowblock_tree",
            "multi_accumulator_3", "strip_mined_4")
 for c in CORPUS:
     for kind, inner in (("csr", "colids"), ("da", "offsets")):
@@ -48,7 +48,7 @@ for rows in (32, 64):
         assert np.array_equal(y.cpu().numpy(), ref)
 for max_len, medium_len in ((1, 1), (3, 3), (5, 40), (40, 254)):
     dm.build_slices(max_len, medium_len)
-    for v in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred"):
+    for v in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"):
         y = dg.spmv(dm, x, variant=v)
         assert np.array_equal(y.cpu().numpy(), ref)
 for v in kernels:

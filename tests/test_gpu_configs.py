@@ -60,7 +60,7 @@ def test_c3_full_size(cuda):
     assert torch.equal(yd, yc)  # naive CSR == naive DA bit-exact (reference crit 4)
     # every exact kernel (both layouts) gives the same bits at full size
     for dm in (da, csr):
-        for kernel in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "wstream", "scalar"):
+        for kernel in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe", "wstream", "scalar"):
             yk = torch.empty(n, dtype=torch.float64, device=cuda)
             dm.spmv_into(x, yk, 1.0, 0.0, kernel, 0)
             assert torch.equal(yk, yd), (dm.kind, kernel)
@@ -101,7 +101,7 @@ def test_c4_rcm_and_skew(cuda):
     assert info["bandwidth_rcm"] == g["bandwidth_rcm"]
     d = dg.to_dacsr(a, 16)
     x = np.random.default_rng(3).uniform(-1, 1, a.ncols)
-    for variant in ("naive", "strip_mined_4", "sliced", "sliced_tma", "sliced_ring", "sliced_pred"):
+    for variant in ("naive", "strip_mined_4", "sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"):
         y = dg.spmv(d, x, variant=variant)
         order = variant if variant in ("naive", "strip_mined_4") else "naive"
         ref = oracle.spmv("da", d.rowptr, d.colids, d.values, x, order=order, threads=8)
