@@ -27,7 +27,7 @@ def test_sumsq_matches_oracle_restatement(cuda):
     assert float(fold_ordered(p).item()) == oracle.fold_ordered(want)
 
 
-@pytest.mark.parametrize("variant", ["naive", "sliced"])
+@pytest.mark.parametrize("variant", ["naive", "sliced", "sliced_pipe"])
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_rank_local_blocks_bit_exact(cuda, world, variant):
     arr = banded_arrays(N, B, LAM, KMAX, SEED, cuda, kinds=("da", "csr"))
