@@ -141,6 +141,10 @@ typedef struct {
   const int64_t* long_rows; /* n_long, ascending                             */
 } dacsr_slices_t;
 
+/* dacsr_plan_t.flags: the SLICED kernels skip the L2 bulk prefetch of the
+ * slice two steps ahead (measured per matrix by DeviceMatrix.autotune). */
+enum { DACSR_PLAN_NO_L2_PREFETCH = 1 };
+
 /* Row-length statistics of rows [row_start, row_end). */
 typedef struct {
   int64_t rows;
@@ -172,7 +176,7 @@ typedef struct {
   int64_t n_complex;
   const int64_t* complex_chunks; /* device, n_complex chunk indices          */
   int32_t ctas_per_sm; /* WSTREAM/SLICED resident CTAs per SM (0 = max)      */
-  int32_t reserved;
+  int32_t flags;       /* DACSR_PLAN_* bits                                  */
   /* SLICED: the layout (its row range must contain the launch's rows).     */
   const dacsr_slices_t* slices;
 } dacsr_plan_t;

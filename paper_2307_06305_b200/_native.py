@@ -31,6 +31,7 @@ VARIANT_CODES = {
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported dtype", 3: "unknown variant/order",
           4: "CUDA error", 5: "plan mismatch"}
 ANALYZE_SCRATCH = 64
+PLAN_NO_L2_PREFETCH = 1  # dacsr_plan_t.flags
 
 _NP_CODE = {"int8": I8, "int16": I16, "int32": I32, "int64": I64, "float32": F32,
             "float64": F64, "float16": F16, "bfloat16": BF16}
@@ -67,7 +68,7 @@ class Plan(ctypes.Structure):
                 ("long_len", ctypes.c_int32), ("block_rows", ctypes.c_void_p),
                 ("chunk_vcap", ctypes.c_int32), ("chunk_rows", ctypes.c_int32),
                 ("n_complex", ctypes.c_int64), ("complex_chunks", ctypes.c_void_p),
-                ("ctas_per_sm", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("ctas_per_sm", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("slices", ctypes.c_void_p)]
 
 

@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
                                        : TMA == 4 ? DACSR_SLICED_PIPE_MINB
                                                   : SlicedTune<VT>::minb)
     sliced_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs, int64_t re,
-                  int side_ctas, int wcap) {
+                  int side_ctas, int wcap, int flags) {
   constexpr int B = SlicedTune<VT>::batch;
   using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
   using SS = SliceStage<CI, VT>;
@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
       mbar_arrive_expect_tx(&bar[slot], vb + ib);
       bulk_copy_g2s(dst, sl.v + q.p0, vb, &bar[slot]);
       bulk_copy_g2s(dst + SS::value_bytes(wcap), sl.ci + q.p0, ib, &bar[slot]);
-    } else if (DACSR_SLICED_PREFETCH) {
+    } else if (DACSR_SLICED_PREFETCH && !(flags & DACSR_PLAN_NO_L2_PREFETCH)) {
       prefetch_l2_bulk(sl.v + q.p0, vb);
       prefetch_l2_bulk(sl.ci + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(CI)) & ~15u);
     }
@@ -1639,7 +1639,8 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, sa, q.rs, q.re, side, wcap);
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, sa, q.rs, q.re, side, wcap,
+                                         static_cast<int>(p->flags));
       if (e != cudaSuccess) {
         set_last_error("sliced_kernel launch", e);
         return DACSR_ERR_CUDA;

@@ -369,7 +369,19 @@ class DeviceMatrix:
             if (k in ("wstream", "rowblock") or k in SLICED_KERNELS) and self.plan is None:
                 continue
             times[k] = timed(k)
-        self.tuned_kernel = min(times, key=times.get)
+        if self._sliced is not None:
+            # the L2 bulk prefetch of the slice two steps ahead helps some
+            # matrices and costs others a few percent: time both
+            self.set_sliced_l2_prefetch(False)
+            for k in ("sliced", "sliced_pipe"):
+                if k in times:
+                    times[k + ":no_l2_prefetch"] = timed(k)
+            self.set_sliced_l2_prefetch(True)
+        best = min(times, key=times.get)
+        if best.endswith(":no_l2_prefetch"):
+            best = best.split(":")[0]
+            self.set_sliced_l2_prefetch(False)
+        self.tuned_kernel = best
         if self.tuned_kernel not in SLICED_KERNELS and self._sliced is not None:
             # the sliced copy of the entries was only built to be timed
             self._sliced = None
@@ -377,6 +389,20 @@ class DeviceMatrix:
             if getattr(self, "_streamed", None) is not None:
                 self._streamed._plans.clear()
         return times
+
+    def set_sliced_l2_prefetch(self, on):
+        """Enable / disable the sliced kernels' L2 bulk prefetch of the slice
+        two steps ahead (dacsr_plan_t.flags)."""
+        if self._sliced is None:
+            return
+        plan = self._sliced[0]
+        if on:
+            plan.flags &= ~_native.PLAN_NO_L2_PREFETCH
+        else:
+            plan.flags |= _native.PLAN_NO_L2_PREFETCH
+        self._launch_cache.clear()
+        if getattr(self, "_streamed", None) is not None:
+            self._streamed._plans.clear()
 
     def set_ctas_per_sm(self, n):
         """Cap WSTREAM's resident CTAs per SM (0 = occupancy maximum)."""

@@ -167,3 +167,19 @@ def test_streamed_host_path_on_slices(cuda, variant):
         dg.spmv(a, x, yp.numpy(), alpha, beta)
         assert np.array_equal(bits(yp.numpy()), bits(ref)), (alpha, beta, "pinned")
     dm.tuned_kernel = None
+
+
+def test_l2_prefetch_flag_keeps_bits(cuda):
+    """dacsr_plan_t.flags (no L2 bulk prefetch) changes timing only."""
+    a = dg.to_dacsr(add_skew_rows(laplacian_2d(256), frac=0.02, alpha=1.2, cap=400, band=200,
+                                  seed=8), 16)
+    dm = DeviceMatrix.from_host(a, cuda)
+    dm.build_slices()
+    x = torch.from_numpy(uniform_x(a.ncols, 3)).to(cuda)
+    ref = oracle.spmv("da", a.rowptr, a.colids, a.values, x.cpu().numpy())
+    for on in (False, True):
+        dm.set_sliced_l2_prefetch(on)
+        for variant in ("sliced", "sliced_pipe", "sliced_pred"):
+            y = dm.spmv_into(x, torch.empty(a.nrows, dtype=torch.float64, device=cuda), 1.0,
+                             0.0, variant)
+            assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (on, variant)
