@@ -349,20 +349,25 @@ class DeviceMatrix:
             # the main/medium split changes the slice widths a warp walks:
             # time the cost model's choice against 8 and 16 (one batch or
             # two per slice) and keep the fastest layout
+            # (timed with SLICED_PIPE, the usual winner, with and without
+            # the L2 prefetch: C5 prefers 16 without it, C2 7 with it)
             model = self.slice_max_len()
             longest = int(self.stats.max_len) if self.stats is not None else 254
+            probe = "sliced_pipe" if "sliced_pipe" in candidates else "sliced"
             tried = {}
             for t in sorted({model, 8, 16}):
                 t = min(t, max(1, longest))
-                if t in tried:
+                if (t, True) in tried:
                     continue
                 self.build_slices(t)
-                tried[t] = timed("sliced")
-            best_t = min(tried, key=tried.get)
+                tried[(t, True)] = timed(probe)
+                self.set_sliced_l2_prefetch(False)
+                tried[(t, False)] = timed(probe)
+            best_t, _ = min(tried, key=tried.get)
             if self._sliced is None or self._sliced[1].max_len != best_t:
                 self.build_slices(best_t)
-            times["sliced"] = tried[best_t]
-            self.slice_max_len_tuned = {int(k): v for k, v in tried.items()}
+            self.slice_max_len_tuned = {f"{k[0]}{'' if k[1] else ':no_l2_prefetch'}": v
+                                        for k, v in tried.items()}
         for k in candidates:
             if k in times:
                 continue
