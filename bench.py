@@ -260,7 +260,8 @@ def suite_line(name, builder):
         fn = lambda: dm.spmv_into(x, y, 1.0, 0.0, kwarm, order)
         warm = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=2, min_epoch_time=0.02,
                            graph=10)
-        dm.autotune(cold=True, x=x)
+        # the layout width was chosen on the (steadier) warm timings
+        dm.autotune(cold=True, x=x, tune_layout=False)
         kname = kernel_for(dm, kname, order)
         fn = lambda: dm.spmv_into(x, y, 1.0, 0.0, kname, order)
         cold = time_kernel(fn, epochs=3, warmup_iters=1, min_epoch_iters=3, min_epoch_time=0.0,
@@ -268,9 +269,31 @@ def suite_line(name, builder):
         out[kind] = {"kernel": kname, "kernel_warm": kwarm, "bytes": traffic, "nnz": dm.nnz,
                      "warm_us": round(warm * 1e6, 2), "warm_gbs": round(traffic / warm / 1e9, 1),
                      "cold_us": round(cold * 1e6, 2), "cold_gbs": round(traffic / cold / 1e9, 1)}
+        if kind == "da":
+            da_choice = (kwarm, kname, dm._sliced[1].max_len if dm._sliced is not None else None,
+                         dm._sliced[0].flags if dm._sliced is not None else 0)
+        elif "da" in out:
+            # the same kernels and slice layout as DA: the ratio then isolates
+            # the format (2- vs 4-byte indices) from kernel selection
+            kw, kc, t_da, flags = da_choice
+            if t_da is not None:
+                dm.build_slices(t_da)
+                dm.set_sliced_l2_prefetch(not (flags & 1))
+            fn = lambda: dm.spmv_into(x, y, 1.0, 0.0, kw, order)
+            w2 = time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=2,
+                             min_epoch_time=0.02, graph=10)
+            fn = lambda: dm.spmv_into(x, y, 1.0, 0.0, kc, order)
+            c2 = time_kernel(fn, epochs=3, warmup_iters=1, min_epoch_iters=3, min_epoch_time=0.0,
+                             cold=True)
+            out[kind]["same_kernels_as_da"] = {"warm_us": round(w2 * 1e6, 2),
+                                               "cold_us": round(c2 * 1e6, 2)}
     if "da" in out and "csr" in out:
         out["uplift_cold"] = round(out["csr"]["cold_us"] / out["da"]["cold_us"], 4)
         out["uplift_predicted"] = round(out["csr"]["bytes"] / out["da"]["bytes"], 4)
+        same = out["csr"].get("same_kernels_as_da")
+        if same:
+            out["uplift_same_kernels_warm"] = round(same["warm_us"] / out["da"]["warm_us"], 4)
+            out["uplift_same_kernels_cold"] = round(same["cold_us"] / out["da"]["cold_us"], 4)
     del mats
     torch.cuda.empty_cache()
     return out

@@ -330,10 +330,12 @@ class DeviceMatrix:
     def autotune(self, candidates=("sliced", "sliced_pipe", "sliced_pred", "sliced_ring",
                                    "sliced_tma", "wstream", "scalar", "rowblock", "staged"),
                  cold=False,
-                 x=None, reps=5):
+                 x=None, reps=5, tune_layout=True):
         """Time the exact naive-order kernels on this matrix and remember the
         fastest for variant "naive"/"auto" (all give bit-identical results,
-        so this only changes speed).  Returns {kernel: seconds}."""
+        so this only changes speed).  With ``tune_layout`` the sliced
+        layout's width (max_len) is chosen too; otherwise the current layout
+        is kept.  Returns {kernel: seconds}."""
         from .harness import time_kernel
         if x is None:
             x = torch.ones(self.ncols, dtype=self.values.dtype, device=self.device)
@@ -345,7 +347,7 @@ class DeviceMatrix:
             return time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
                                min_epoch_time=0.0, cold=cold, graph=0 if cold else reps)
 
-        if "sliced" in candidates and self.plan is not None and self.nnz:
+        if tune_layout and "sliced" in candidates and self.plan is not None and self.nnz:
             # the main/medium split changes the slice widths a warp walks:
             # time the cost model's choice against 8 and 16 (one batch or
             # two per slice) and keep the fastest layout
