@@ -183,3 +183,31 @@ def test_l2_prefetch_flag_keeps_bits(cuda):
             y = dm.spmv_into(x, torch.empty(a.nrows, dtype=torch.float64, device=cuda), 1.0,
                              0.0, variant)
             assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (on, variant)
+
+
+def test_autotune_then_exact(cuda):
+    """autotune() (kernel, slice width, L2-prefetch flag, dropping an unused
+    sliced copy) only changes speed: 'naive' stays bit-exact afterwards."""
+    cases = [c for c in CORPUS if c["nrows"] >= 64][:6]
+    cases.append(None)  # a skewed matrix with medium and long rows
+    for c in cases:
+        if c is None:
+            a = dg.to_dacsr(add_skew_rows(laplacian_2d(128), frac=0.02, alpha=1.2, cap=500,
+                                          band=300, seed=5), 16)
+            x_h = uniform_x(a.ncols, 6)
+            y0 = np.zeros(a.nrows)
+            alpha, beta, want = 1.0, 0.0, None
+        else:
+            a = host_matrix(c, "da")
+            x_h, y0, alpha, beta, want = c["x"], c["y0"], c["alpha"], c["beta"], c["y_naive"]
+        dm = DeviceMatrix.from_host(a, cuda)
+        x = torch.from_numpy(np.ascontiguousarray(x_h)).to(cuda)
+        for cold in (False, True):
+            dm.autotune(cold=cold, x=x, reps=2)
+            assert dm.tuned_kernel in dg.GPU_VARIANTS
+            y = torch.from_numpy(np.ascontiguousarray(y0).copy()).to(cuda)
+            dg.spmv(dm, x, y, alpha, beta, "naive")
+            ref = want if want is not None else oracle.spmv(
+                "da", a.rowptr, a.colids, a.values, np.asarray(x_h), np.asarray(y0).copy(),
+                alpha, beta)
+            assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (dm.tuned_kernel, cold)
