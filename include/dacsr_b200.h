@@ -80,8 +80,12 @@ enum {
   DACSR_VARIANT_SLICED_PRED = 13, /* SLICED + x gathers issued at the offsets of */
                               /* the warp's previous slice (stencil-like rows), */
                               /* re-gathered when the guess was wrong          */
-  DACSR_VARIANT_SLICED_PIPE = 14 /* SLICED with the next slice's offsets loaded  */
+  DACSR_VARIANT_SLICED_PIPE = 14, /* SLICED with the next slice's offsets loaded */
                               /* while this slice's gathers are in flight       */
+  DACSR_VARIANT_TILED = 15    /* band-tiled layout (plan->tiles): x staged in    */
+                              /* shared memory tile by tile (TMA bulk copies),  */
+                              /* lane per 16 rows, exact naive order; for wide  */
+                              /* random bands (C3, C5)                          */
 };
 
 /* A matrix in CSR (absolute colids) or DA-CSR (colids = col - row) layout.
@@ -141,6 +145,48 @@ typedef struct {
   const int64_t* long_rows; /* n_long, ascending                             */
 } dacsr_slices_t;
 
+/* Band-tiled device layout of rows [row_start, row_end) (TILED kernel) — a
+ * derived copy of the entries for matrices whose rows spread over a wide
+ * band (x gathers would miss L1 one sector per entry).
+ *
+ * Rows come in groups of 512: lane l (0..31) of group g holds rows
+ * row_start + 512g + 32j + l, j = 0..15.  Columns come in tiles of
+ * tile_cols: tile t = [col0 + t*tile_cols, col0 + (t+1)*tile_cols).  Group g
+ * spans tiles tile_lo[g] .. tile_lo[g] + (cnt_ptr[g+1] - cnt_ptr[g]) - 1; for
+ * its k-th tile, counts[(cnt_ptr[g] + k) * 32 + l] holds 16 nibbles, nibble j
+ * = the entries of row j of lane l whose column falls in the tile (0..15).
+ * The group's entries start at ent_ptr[g], tile after tile.  Inside a tile,
+ * lane l's entries (its rows j = 0..15 in order, each row's entries in
+ * column order) form a list L_l, stored "step-major": entry k of L_l sits at
+ * tile_base + sum_{k' < k} |{l' : |L_l'| > k'}| + |{l' < l : |L_l'| > k}|,
+ * so the lanes of a warp read step k of their lists as one packed run (no
+ * padding).  Entries are bit-for-bit copies; every row's entries keep their
+ * order, so a lane folding its list in order reproduces the naive sum.
+ * Rows with more than 15 entries inside one tile are left out (counts 0,
+ * bit j of skip[32g + l] set) and listed ascending in ovf_rows; the kernel
+ * reduces them warp by warp from the CSR arrays.  inner / values carry 16
+ * padding entries past `total` (bulk L2 prefetches may round up). */
+typedef struct {
+  int64_t row_start;
+  int64_t row_end;
+  int64_t ngroups;          /* ceil((row_end - row_start) / 512)            */
+  int64_t col0;             /* first column of tile 0 (= cmin)              */
+  int64_t cmax;             /* last column any entry uses                   */
+  int32_t tile_cols;        /* columns per tile (x tile = tile_cols values) */
+  int32_t reserved;
+  int64_t total;            /* entries in the layout                        */
+  int64_t nblocks;          /* cnt_ptr[ngroups]                             */
+  const int64_t* ent_ptr;   /* ngroups + 1                                  */
+  const int64_t* cnt_ptr;   /* ngroups + 1                                  */
+  const int32_t* tile_lo;   /* ngroups                                      */
+  const uint64_t* counts;   /* nblocks * 32                                 */
+  const uint16_t* skip;     /* ngroups * 32                                 */
+  const void* inner;        /* total + 16, the matrix's colids dtype        */
+  const void* values;       /* total + 16, the matrix's values dtype        */
+  int64_t n_ovf;
+  const int64_t* ovf_rows;  /* n_ovf, ascending                             */
+} dacsr_tiles_t;
+
 /* dacsr_plan_t.flags: the SLICED kernels skip the L2 bulk prefetch of the
  * slice two steps ahead (measured per matrix by DeviceMatrix.autotune). */
 enum { DACSR_PLAN_NO_L2_PREFETCH = 1 };
@@ -179,6 +225,8 @@ typedef struct {
   int32_t flags;       /* DACSR_PLAN_* bits                                  */
   /* SLICED: the layout (its row range must contain the launch's rows).     */
   const dacsr_slices_t* slices;
+  /* TILED: the layout (its row range must contain the launch's rows).      */
+  const dacsr_tiles_t* tiles;
 } dacsr_plan_t;
 
 const char* dacsr_version(void);
@@ -231,6 +279,25 @@ int dacsr_slices_fill(const dacsr_matrix_t* a, const dacsr_slices_t* s,
                       const int64_t* medium_ptr_dev, const int64_t* long_ptr_dev, void* stream);
 int dacsr_slices_medium_count(const dacsr_slices_t* s, int32_t* m_slot_counts_dev, void* stream);
 int dacsr_slices_medium_fill(const dacsr_matrix_t* a, const dacsr_slices_t* s, void* stream);
+
+/* Band-tiled layout builder (warp per 512-row group; the caller scans the
+ * per-group counts into int64 prefixes between the passes and sizes the
+ * buffers from the totals).
+ * 1. dacsr_tiles_extent: out2_dev[0] = min column, out2_dev[1] = max column
+ *    of the entries of rows [row_start, row_end) (INT64_MAX / INT64_MIN if
+ *    none); stream-ordered.
+ * 2. dacsr_tiles_count (t->row_start/row_end/ngroups/col0/tile_cols set):
+ *    per group nt_counts[g] = tiles spanned, ent_counts[g] = entries kept,
+ *    ovf_counts[g] = rows left out; t->tile_lo and t->skip filled.
+ * 3. dacsr_tiles_fill (every t field set; ovf_ptr = scanned ovf_counts):
+ *    counts, inner, values, ovf_rows.
+ * 64 <= tile_cols <= 65536, a multiple of 16. */
+int dacsr_tiles_extent(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end,
+                       int64_t* out2_dev, void* stream);
+int dacsr_tiles_count(const dacsr_matrix_t* a, const dacsr_tiles_t* t, int32_t* nt_counts_dev,
+                      int32_t* ent_counts_dev, int32_t* ovf_counts_dev, void* stream);
+int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int64_t* ovf_ptr_dev,
+                     void* stream);
 
 /* Variant the library would run for DACSR_VARIANT_AUTO. */
 int32_t dacsr_select_variant(const dacsr_stats_t* stats, int32_t order);

@@ -26,7 +26,7 @@ KIND_CSR, KIND_DA = 0, 1
 ORDER_NAIVE, ORDER_MACC3, ORDER_STRIP4, ORDER_TREE = range(4)
 VARIANT_CODES = {
     "auto": 0, "rowblock": 1, "scalar": 2, "vector2": 3, "vector4": 4, "vector8": 5,
-    "vector16": 6, "warp": 7, "staged": 8, "wstream": 9, "sliced": 10, "sliced_tma": 11, "sliced_ring": 12, "sliced_pred": 13, "sliced_pipe": 14,
+    "vector16": 6, "warp": 7, "staged": 8, "wstream": 9, "sliced": 10, "sliced_tma": 11, "sliced_ring": 12, "sliced_pred": 13, "sliced_pipe": 14, "tiled": 15,
 }
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported dtype", 3: "unknown variant/order",
           4: "CUDA error", 5: "plan mismatch"}
@@ -69,7 +69,7 @@ class Plan(ctypes.Structure):
                 ("chunk_vcap", ctypes.c_int32), ("chunk_rows", ctypes.c_int32),
                 ("n_complex", ctypes.c_int64), ("complex_chunks", ctypes.c_void_p),
                 ("ctas_per_sm", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("slices", ctypes.c_void_p)]
+                ("slices", ctypes.c_void_p), ("tiles", ctypes.c_void_p)]
 
 
 class Slices(ctypes.Structure):
@@ -84,6 +84,19 @@ class Slices(ctypes.Structure):
                 ("m_slice_ptr", ctypes.c_void_p), ("m_inner", ctypes.c_void_p),
                 ("m_values", ctypes.c_void_p), ("n_long", ctypes.c_int64),
                 ("long_rows", ctypes.c_void_p)]
+
+
+class Tiles(ctypes.Structure):
+    """dacsr_tiles_t: the band-tiled device layout (512-row groups x column tiles)."""
+    _fields_ = [("row_start", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("ngroups", ctypes.c_int64), ("col0", ctypes.c_int64), ("cmax", ctypes.c_int64),
+                ("tile_cols", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("total", ctypes.c_int64), ("nblocks", ctypes.c_int64),
+                ("ent_ptr", ctypes.c_void_p), ("cnt_ptr", ctypes.c_void_p),
+                ("tile_lo", ctypes.c_void_p), ("counts", ctypes.c_void_p),
+                ("skip", ctypes.c_void_p), ("inner", ctypes.c_void_p),
+                ("values", ctypes.c_void_p), ("n_ovf", ctypes.c_int64),
+                ("ovf_rows", ctypes.c_void_p)]
 
 
 def typed_kernel_names():
@@ -110,6 +123,9 @@ _SIGNATURES = {
     "dacsr_slices_fill": ([_P(Matrix), _P(Slices), _vp, _vp, _vp], ctypes.c_int),
     "dacsr_slices_medium_count": ([_P(Slices), _vp, _vp], ctypes.c_int),
     "dacsr_slices_medium_fill": ([_P(Matrix), _P(Slices), _vp], ctypes.c_int),
+    "dacsr_tiles_extent": ([_P(Matrix), _i64, _i64, _vp, _vp], ctypes.c_int),
+    "dacsr_tiles_count": ([_P(Matrix), _P(Tiles), _vp, _vp, _vp, _vp], ctypes.c_int),
+    "dacsr_tiles_fill": ([_P(Matrix), _P(Tiles), _vp, _vp], ctypes.c_int),
     "dacsr_plan_chunks": ([_P(Matrix), _i64, _i64, _i32, _i32, _vp, _vp, _P(Plan), _vp],
                           ctypes.c_int),
     "dacsr_spmv": ([_P(Matrix), _P(Plan), _i32, _i32, _vp, _i64, _vp, _d, _d, _i64, _i64, _vp],

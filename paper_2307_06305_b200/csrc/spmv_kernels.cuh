@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -1293,6 +1294,8 @@ __global__ void classify_chunks_kernel(const RP* __restrict__ rp, int64_t rs, in
   }
 }
 
+#include "tiled.cuh"
+
 // one launch request (dacsr_spmv arguments after validation)
 struct Req {
   const dacsr_plan_t* plan;
@@ -1662,6 +1665,45 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
         return DACSR_ERR_CUDA;
       }
       return check_launch("sliced_kernel");
+    }
+    case DACSR_VARIANT_TILED: {
+      const dacsr_plan_t* p = q.plan;
+      if (!p || !p->tiles) return DACSR_ERR_PLAN;
+      const dacsr_tiles_t* td = p->tiles;
+      if (q.rs < td->row_start || q.re > td->row_end || td->tile_cols < 64 ||
+          td->tile_cols > 65536 || (td->tile_cols & 15) ||
+          td->ngroups != (td->row_end - td->row_start + 511) / 512 ||
+          (td->ngroups > 0 && (!td->ent_ptr || !td->cnt_ptr || !td->tile_lo || !td->skip)) ||
+          (td->nblocks > 0 && !td->counts) || (td->total > 0 && (!td->inner || !td->values)) ||
+          (td->n_ovf > 0 && !td->ovf_rows) || (a->nnz > 0 && (!a->colids || !a->values)))
+        return DACSR_ERR_PLAN;
+      if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
+        // the tiled fold specialises the naive order; the others run row blocks
+        Req r2 = q;
+        r2.variant = p->block_rows && p->row_start == q.rs && p->row_end == q.re
+                         ? DACSR_VARIANT_ROWBLOCK
+                         : DACSR_VARIANT_STAGED;
+        return launch<KIND, RP, CI, VT>(a, r2);
+      }
+      const int xbuf = td->tile_cols + static_cast<int>(16 / sizeof(VT));
+      const size_t smem = tiled_smem_bytes<VT>(xbuf);
+      const int threads = 32 * (kTileWarps + 1);
+      auto kern = tiled_kernel<KIND, RP, CI, VT>;
+      int per_sm = cached_per_sm(kern, threads, smem);
+      if (per_sm < 0) return check_launch("tiled launch config");
+      const int64_t g_first = (q.rs - td->row_start) / 512;
+      const int64_t g_last = (q.re - td->row_start + 511) / 512;
+      const int64_t nchunks = (g_last - g_first + kTileWarps - 1) / kTileWarps;
+      const int64_t grid = std::max<int64_t>(
+          1, std::min<int64_t>(std::max<int64_t>(nchunks, (td->n_ovf + kTileWarps - 1) / kTileWarps),
+                               static_cast<int64_t>(sms) * per_sm));
+      TileArgs<CI, VT> ta{td->ent_ptr, td->cnt_ptr, td->tile_lo, td->counts, td->skip,
+                          static_cast<const CI*>(td->inner), static_cast<const VT*>(td->values),
+                          td->ovf_rows, td->row_start, td->col0, td->cmax, td->total, td->n_ovf,
+                          td->tile_cols};
+      kern<<<static_cast<unsigned>(grid), threads, smem, q.stream>>>(m, s, ta, g_first, g_last,
+                                                                     q.rs, q.re, xbuf);
+      return check_launch("tiled_kernel");
     }
     default:
       return DACSR_ERR_VARIANT;

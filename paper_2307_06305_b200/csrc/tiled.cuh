@@ -1,0 +1,384 @@
+// TILED: the band-tiled SpMV kernel (layout: csrc/tiles.cu, dacsr_tiles_t).
+//
+// Included by spmv_kernels.cuh inside namespace dacsr (needs Mat, Scal,
+// warp_long_row, ldcs, prefetch_l2_bulk).
+//
+// One CTA per SM, persistent over chunks of kTileWarps 512-row groups
+// (8192 rows).  Warp kTileWarps is the producer: it walks the chunk's
+// column tiles in order and streams each tile of x into one of two
+// shared-memory buffers with a TMA bulk copy (cp.async.bulk, full/empty
+// mbarriers).  Consumer warp w owns group w of the chunk: lane l holds rows
+// 32j + l (j = 0..15) and, per tile, folds its list of entries (its rows in
+// order, each row's entries of the tile in column order) with the x values
+// read from shared memory — random 8-byte reads that cost a few bank
+// wavefronts per warp instead of a 32-byte L2 sector each.  The row sums
+// live in shared memory between tiles (a lane swaps its running sum when it
+// moves to its next row), so each row is folded from +0.0 in column order:
+// the reference's naive order, bit for bit (_numba_kernels.py:82-91).
+//
+// The operator is read once, step-major packed (coalesced runs), with
+// evict-first loads; the next tile's segment is pulled into L2 by a bulk
+// prefetch one tile ahead.  Rows the layout left out (more than 15 entries
+// inside one tile) are reduced warp by warp from the CSR arrays at the end.
+#pragma once
+
+
+constexpr int kTileWarps = 16;  // consumer warps (groups) per CTA
+constexpr int kTileRows = 16;   // rows per lane
+#ifndef DACSR_TILED_BATCH
+#define DACSR_TILED_BATCH 8     // steps whose entries are loaded together
+#endif
+
+template <class CI, class VT>
+struct TileArgs {
+  const int64_t* __restrict__ ent_ptr;
+  const int64_t* __restrict__ cnt_ptr;
+  const int32_t* __restrict__ tile_lo;
+  const uint64_t* __restrict__ counts;
+  const uint16_t* __restrict__ skip;
+  const CI* __restrict__ ci;
+  const VT* __restrict__ v;
+  const int64_t* __restrict__ ovf;
+  int64_t row0, col0, cmax, total, n_ovf;
+  int T;
+};
+
+// shared memory: two x buffers of xbuf elements, the row sums, 4 mbarriers
+template <class VT>
+__host__ __device__ constexpr size_t tiled_xbuf_bytes(int xbuf) {
+  return (static_cast<size_t>(xbuf) * sizeof(VT) + 127) & ~size_t(127);
+}
+template <class VT>
+__host__ __device__ constexpr size_t tiled_smem_bytes(int xbuf) {
+  return 2 * tiled_xbuf_bytes<VT>(xbuf) + size_t(kTileWarps) * (kTileRows + 1) * 32 * 8 + 64;
+}
+
+__device__ __forceinline__ int nibble_sum(uint64_t v) {
+  const uint64_t s = (v & 0x0F0F0F0F0F0F0F0Full) + ((v >> 4) & 0x0F0F0F0F0F0F0F0Full);
+  return static_cast<int>((s * 0x0101010101010101ull) >> 56);
+}
+
+// shared-memory loads / stores through 32-bit shared addresses
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+template <class VT>
+__device__ __forceinline__ VT lds_val(uint32_t a);
+template <>
+__device__ __forceinline__ double lds_val<double>(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+template <>
+__device__ __forceinline__ float lds_val<float>(uint32_t a) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+template <>
+__device__ __forceinline__ __half lds_val<__half>(uint32_t a) {
+  unsigned short v;
+  asm("ld.shared.b16 %0, [%1];" : "=h"(v) : "r"(a));
+  return __ushort_as_half(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 lds_val<__nv_bfloat16>(uint32_t a) {
+  unsigned short v;
+  asm("ld.shared.b16 %0, [%1];" : "=h"(v) : "r"(a));
+  return __ushort_as_bfloat16(v);
+}
+
+// &base[o] for a 32-bit unsigned offset as one IMAD.WIDE.U32
+template <class T>
+__device__ __forceinline__ const T* elem_addr_u32(const T* base, uint32_t o) {
+  const T* p;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(o), "n"(static_cast<int>(sizeof(T))), "l"(base));
+  return p;
+}
+
+// predicated evict-first load (asm volatile: issued in program order, so a
+// batch's loads all leave before the batch folds); 0 when !pred
+template <class T>
+struct LdCs;
+#define DACSR_LDCS_PRED(T, R, C, SUF)                                                  \
+  template <>                                                                          \
+  struct LdCs<T> {                                                                     \
+    using reg = R;                                                                     \
+    __device__ __forceinline__ static R load(const T* p, bool pred) {                  \
+      R v = 0;                                                                         \
+      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cs." SUF \
+                   " %0, [%1];\n\t}"                                                  \
+                   : "+" C(v)                                                          \
+                   : "l"(p), "r"(static_cast<unsigned>(pred)));                        \
+      return v;                                                                        \
+    }                                                                                  \
+  };
+DACSR_LDCS_PRED(int8_t, int, "r", "s8")
+DACSR_LDCS_PRED(int16_t, int, "r", "s16")
+DACSR_LDCS_PRED(int32_t, int, "r", "s32")
+DACSR_LDCS_PRED(int64_t, long long, "l", "s64")
+DACSR_LDCS_PRED(double, double, "d", "f64")
+DACSR_LDCS_PRED(float, float, "f", "f32")
+DACSR_LDCS_PRED(unsigned short, unsigned short, "h", "b16")
+#undef DACSR_LDCS_PRED
+template <class T, class OUT>
+__device__ __forceinline__ OUT ld_cs_pred(const T* p, bool pred) {
+  if constexpr (std::is_same<T, __half>::value)
+    return __ushort_as_half(LdCs<unsigned short>::load(reinterpret_cast<const unsigned short*>(p), pred));
+  else if constexpr (std::is_same<T, __nv_bfloat16>::value)
+    return __ushort_as_bfloat16(
+        LdCs<unsigned short>::load(reinterpret_cast<const unsigned short*>(p), pred));
+  else
+    return static_cast<OUT>(LdCs<T>::load(p, pred));
+}
+
+// mbarrier wait with a short back-off (the producer polls for whole tiles)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+}
+
+template <int KIND, class RP, class CI, class VT>
+__global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
+    tiled_kernel(Mat<KIND, RP, CI, VT> m, Scal s, TileArgs<CI, VT> ta, int64_t g_first,
+                 int64_t g_last, int64_t rs, int64_t re, int xbuf) {
+  using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
+  constexpr int U = DACSR_TILED_BATCH;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  VT* const xs = reinterpret_cast<VT*>(dsm);
+  const size_t xstride = tiled_xbuf_bytes<VT>(xbuf) / sizeof(VT);
+  double* const accs = reinterpret_cast<double*>(dsm + 2 * tiled_xbuf_bytes<VT>(xbuf));
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(accs + kTileWarps * (kTileRows + 1) * 32);
+  uint64_t* const full = bars;
+  uint64_t* const empty = bars + 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], kTileWarps);
+    mbar_init(&empty[1], kTileWarps);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t nchunks = (g_last - g_first + kTileWarps - 1) / kTileWarps;
+  const VT* const xb = m.x + m.xoff;
+
+  // tiles spanned by chunk c: lanes k < kTileWarps read group k's range
+  auto chunk_range = [&](int64_t c, int64_t& tlo, int64_t& thi) {
+    const int64_t g = g_first + c * kTileWarps + lane;
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    if (lane < kTileWarps && g < g_last) {
+      const int64_t nt = ldg(ta.cnt_ptr + g + 1) - ldg(ta.cnt_ptr + g);
+      if (nt > 0) {
+        lo = ldg(ta.tile_lo + g);
+        hi = lo + nt - 1;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    tlo = lo;
+    thi = hi;
+  };
+  // x element i of a tile buffer holds column base + i, base = cs - shift
+  // (the bulk copy starts at the 16-byte boundary at or below x[cs])
+  auto tile_shift = [&](int64_t cs) {
+    return static_cast<int>((reinterpret_cast<uintptr_t>(xb + cs) & 15) / sizeof(VT));
+  };
+
+  if (warp == kTileWarps) {  // ---------------------------------- producer
+    uint32_t it = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      int64_t tlo, thi;
+      chunk_range(c, tlo, thi);
+      for (int64_t t = tlo; t <= thi; ++t, ++it) {
+        const int b = it & 1;
+        if (lane == 0) {
+          if (it >= 2) mbar_wait_backoff(&empty[b], ((it >> 1) - 1) & 1);
+          const int64_t cs = ta.col0 + t * ta.T;
+          const int64_t ce = min64(cs + ta.T, ta.cmax + 1);
+          const int shift = tile_shift(cs);
+          const VT* src = xb + cs - shift;  // 16-byte aligned
+          const int64_t n = ce - cs + shift;
+          DACSR_CHECK(n > 0 && n <= xbuf);
+          const uint32_t main = static_cast<uint32_t>((n * sizeof(VT)) & ~int64_t(15));
+          VT* dst = xs + b * xstride;
+          // the last < 16 bytes with plain loads (the bulk copy must not
+          // read past x's last element)
+          for (int64_t q = main / sizeof(VT); q < n; ++q) dst[q] = src[q];
+          mbar_arrive_expect_tx(&full[b], main);
+          if (main) bulk_copy_g2s(dst, src, main, &full[b]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  // row sums: lane l's row j at wacc + (32 j + l) * 8; row 16 is a dummy
+  // slot (the first "switch" of a tile parks the empty running sum there)
+  double* const wacc = accs + warp * (kTileRows + 1) * 32;
+  const uint32_t wa = smem_addr(wacc) + 8u * lane;
+  const uint32_t xs0 = smem_addr(xs);
+  const size_t vpad = ta.total + 16;  // inner / values carry 16 padding entries
+  auto prefetch_segment = [&](int64_t p0, int n) {
+    if (lane != 0 || n <= 0) return;
+    const uintptr_t v0 = reinterpret_cast<uintptr_t>(ta.v + p0) & ~uintptr_t(15);
+    const uintptr_t v1 = min(reinterpret_cast<uintptr_t>(ta.v + p0 + n) + 15,
+                             reinterpret_cast<uintptr_t>(ta.v + vpad)) & ~uintptr_t(15);
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(ta.ci + p0) & ~uintptr_t(15);
+    const uintptr_t i1 = min(reinterpret_cast<uintptr_t>(ta.ci + p0 + n) + 15,
+                             reinterpret_cast<uintptr_t>(ta.ci + vpad)) & ~uintptr_t(15);
+    if (v1 > v0) prefetch_l2_bulk(reinterpret_cast<const void*>(v0), static_cast<uint32_t>(v1 - v0));
+    if (i1 > i0) prefetch_l2_bulk(reinterpret_cast<const void*>(i0), static_cast<uint32_t>(i1 - i0));
+  };
+  uint32_t it = 0;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    int64_t tlo, thi;
+    chunk_range(c, tlo, thi);
+    const int64_t g = g_first + c * kTileWarps + warp;
+    const bool has = g < g_last;
+    int64_t gtlo = 0, gnt = 0, cbase = 0, pos = 0;
+    if (has) {
+      gtlo = ldg(ta.tile_lo + g);
+      cbase = ldg(ta.cnt_ptr + g);
+      gnt = ldg(ta.cnt_ptr + g + 1) - cbase;
+      pos = ldg(ta.ent_ptr + g);
+    }
+#pragma unroll
+    for (int j = 0; j < kTileRows; ++j) sts_f64(wa + 256u * j, 0.0);
+    uint64_t cn0 = gnt > 0 ? ldg(ta.counts + cbase * 32 + lane) : 0;
+    uint64_t cn1 = gnt > 1 ? ldg(ta.counts + (cbase + 1) * 32 + lane) : 0;
+    if (gnt > 0)
+      prefetch_segment(pos, __reduce_add_sync(0xffffffffu, static_cast<unsigned>(nibble_sum(cn0))));
+    // rows of lane l: row0 + 512g + 32j + l
+    const int64_t lrow = ta.row0 + 512 * g + lane;
+    for (int64_t t = tlo; t <= thi; ++t, ++it) {
+      const int b = it & 1;
+      const int64_t k = t - gtlo;
+      const bool mine = has && k >= 0 && k < gnt;
+      uint64_t cur = 0;
+      int total = 0, here = 0;
+      if (mine) {
+        cur = cn0;
+        cn0 = cn1;
+        cn1 = k + 2 < gnt ? ldg(ta.counts + (cbase + k + 2) * 32 + lane) : 0;
+        total = nibble_sum(cur);
+        here = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(total)));
+        if (k + 1 < gnt)
+          prefetch_segment(pos + here,
+                           __reduce_add_sync(0xffffffffu, static_cast<unsigned>(nibble_sum(cn0))));
+      }
+      mbar_wait(&full[b], (it >> 1) & 1);
+      if (mine) {
+        const int64_t cs = ta.col0 + t * ta.T;
+        const int64_t d = cs - tile_shift(cs);  // column of x buffer element 0
+        const uint32_t xsa = xs0 + static_cast<uint32_t>(b * xstride * sizeof(VT));
+        // DA: x of entry (row j, offset o) at xr + o * sizeof(VT), xr = &xbuf[row - d];
+        // CSR: at xc + c * sizeof(VT), xc = &xbuf[-d] (32-bit wrap-around arithmetic)
+        const uint32_t xr0 = xsa + static_cast<uint32_t>((lrow - d) * static_cast<int64_t>(sizeof(VT)));
+        const uint32_t xc = xsa - static_cast<uint32_t>(d * static_cast<int64_t>(sizeof(VT)));
+        const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
+        // rows of this tile with entries (bit j), consumed in order
+        uint32_t nz = 0;
+#pragma unroll
+        for (int j = 0; j < kTileRows; ++j) nz |= ((cur >> (4 * j)) & 15u) ? (1u << j) : 0u;
+        int rem = 0;
+        uint32_t acc_a = wa + 32u * 8u * kTileRows;  // dummy slot
+        uint32_t xr = xr0;
+        double acc = 0.0;
+        const VT* vt = ta.v + pos;
+        const CI* ct = ta.ci + pos;
+        // opaque bases: each load address is then one IMAD.WIDE.U32 off the
+        // 32-bit step offset (nvcc otherwise re-derives 64-bit index sums)
+        asm("" : "+l"(vt));
+        asm("" : "+l"(ct));
+        uint32_t lp = 0;
+        // batch of U steps: positions from the step ballots, then every
+        // operator load of the batch issued (predicated asm, program order)
+        auto load_batch = [&](int k0, OT* off, VT* val) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool act = k0 + u < total;
+            const unsigned msk = __ballot_sync(0xffffffffu, act);
+            const uint32_t o = lp + __popc(msk & below);
+            lp += __popc(msk);
+            DACSR_CHECK(!act || pos + o < ta.total);
+            off[u] = ld_cs_pred<CI, OT>(elem_addr_u32(ct, o), act);
+            val[u] = ld_cs_pred<VT, VT>(elem_addr_u32(vt, o), act);
+          }
+        };
+        auto fold_batch = [&](int k0, const OT* off, const VT* val) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool act = k0 + u < total;
+            const bool sw = act && rem == 0;  // this lane's next row of the tile
+            if (sw) {
+              sts_f64(acc_a, acc);
+              const int j = __ffs(nz) - 1;
+              nz &= nz - 1;
+              rem = static_cast<int>((cur >> (4 * j)) & 15u);
+              acc_a = wa + 256u * j;
+              acc = lds_f64(acc_a);
+              xr = xr0 + static_cast<uint32_t>(32 * j * sizeof(VT));
+            }
+            const uint32_t xa = KIND == DACSR_KIND_DA
+                                    ? xr + static_cast<uint32_t>(static_cast<int>(off[u]) * static_cast<int>(sizeof(VT)))
+                                    : xc + static_cast<uint32_t>(off[u] * static_cast<OT>(sizeof(VT)));
+            DACSR_CHECK(!act || (xa >= xsa && xa < xsa + xbuf * sizeof(VT)));
+            const double p = act ? product(val[u], lds_val<VT>(xa)) : 0.0;
+            acc = __dadd_rn(acc, p);  // +0 for idle steps: acc never holds -0
+            rem -= act ? 1 : 0;
+          }
+        };
+        // two batches in flight: batch i+1's loads are issued before batch i folds
+        OT offA[U], offB[U];
+        VT valA[U], valB[U];
+        int k0 = 0;
+        if (kmax > 0) load_batch(0, offA, valA);
+        while (k0 < kmax) {
+          if (k0 + U < kmax) load_batch(k0 + U, offB, valB);
+          fold_batch(k0, offA, valA);
+          k0 += U;
+          if (k0 >= kmax) break;
+          if (k0 + U < kmax) load_batch(k0 + U, offA, valA);
+          fold_batch(k0, offB, valB);
+          k0 += U;
+        }
+        sts_f64(acc_a, acc);
+        pos += lp;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+    }
+    // the chunk's rows: y = alpha * sum (+ beta * y)
+    if (has) {
+      const unsigned sk = ldg(ta.skip + 32 * g + lane);
+#pragma unroll 4
+      for (int j = 0; j < kTileRows; ++j) {
+        const int64_t r = lrow + 32 * j;
+        if (r >= rs && r < re && !((sk >> j) & 1u))
+          epilogue(m.y, r, lds_f64(wa + 256u * j), s.alpha, s.beta);
+      }
+    }
+    __syncwarp();
+  }
+  // rows left out of the layout: warp per row from the CSR arrays
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * kTileWarps + warp; w < ta.n_ovf;
+       w += static_cast<int64_t>(gridDim.x) * kTileWarps) {
+    const int64_t r = ldg(ta.ovf + w);
+    if (r < rs || r >= re) continue;
+    const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1);
+    __syncwarp();
+    warp_long_row(m, s, r, b, e, static_cast<const VT*>(nullptr), static_cast<const CI*>(nullptr),
+                  0, 0, lane, wacc);
+  }
+}
+

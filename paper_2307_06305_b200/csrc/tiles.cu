@@ -1,0 +1,345 @@
+// Builder of the band-tiled device layout (dacsr_tiles_t, include/dacsr_b200.h).
+//
+// For a wide random band (C3/C5: offsets uniform over +-32767) every x
+// gather of the row-major kernels is its own 32-byte sector of L2, and the
+// L1TEX pipe retires about one such gather per SM clock — the kernel then
+// runs at a third of HBM speed.  The TILED kernel stages x in shared memory
+// one column tile at a time (TMA bulk copies) and folds, for each tile, the
+// entries of its rows that fall inside it; the layout built here is the same
+// entries re-laid in exactly that consumption order:
+//
+//   group g (512 rows: lane l holds rows 512g + 32j + l, j = 0..15)
+//     tile t (tile_lo[g] ..):  counts[32]  — lane l: 16 nibbles (entries of
+//                                           its row j inside the tile)
+//                              entries     — lane lists L_l stored
+//                                           step-major (step k: the k-th
+//                                           entry of every lane whose list
+//                                           is longer than k, lanes
+//                                           ascending)
+//
+// A row's entries stay in column order (tiles ascend, and inside a tile its
+// entries are consecutive in its lane's list), so each lane folds every row
+// in the reference's naive order (_numba_kernels.py:82-91).  Entries are
+// copied as raw bits.
+//
+// Passes (warp per group): extent (min / max column), count, fill.
+
+#include <algorithm>
+#include <climits>
+
+#include "device_common.cuh"
+
+namespace dacsr {
+namespace {
+
+constexpr int kGroupRows = 512;
+constexpr int kRowsPerLane = 16;
+
+template <int KIND, class CI>
+__device__ __forceinline__ int64_t entry_col(int64_t r, CI c) {
+  return KIND == DACSR_KIND_DA ? r + static_cast<int64_t>(c) : static_cast<int64_t>(c);
+}
+
+__global__ void extent_init_kernel(long long* out) {
+  out[0] = LLONG_MAX;
+  out[1] = LLONG_MIN;
+}
+
+template <int KIND, class RP, class CI>
+__global__ void extent_kernel(const RP* __restrict__ rp, const CI* __restrict__ ci, int64_t rs,
+                              int64_t re, long long* out) {
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  for (int64_t r = rs + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < re;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = static_cast<int64_t>(rp[r]), e = static_cast<int64_t>(rp[r + 1]);
+    if (e > b) {
+      lo = min(lo, static_cast<long long>(entry_col<KIND>(r, ci[b])));
+      hi = max(hi, static_cast<long long>(entry_col<KIND>(r, ci[e - 1])));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+
+struct TileGeom {
+  int64_t rs, re, col0;
+  int T;
+  __device__ __forceinline__ int64_t tile(int64_t c) const { return (c - col0) / T; }
+};
+
+// Per group: tiles spanned, entries kept, rows left out (some tile holds
+// more than 15 of their entries); tile_lo and the skip masks.
+template <int KIND, class RP, class CI>
+__global__ void tiles_count_kernel(const RP* __restrict__ rp, const CI* __restrict__ ci,
+                                   TileGeom geo, int64_t ngroups, int32_t* __restrict__ nt_counts,
+                                   int32_t* __restrict__ ent_counts,
+                                   int32_t* __restrict__ ovf_counts, int32_t* __restrict__ tile_lo,
+                                   uint16_t* __restrict__ skip) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < ngroups;
+       g += nw) {
+    int64_t tmin = INT64_MAX, tmax = -1;
+    int kept = 0, ovf = 0;
+    unsigned sk = 0;
+    for (int j = 0; j < kRowsPerLane; ++j) {
+      const int64_t r = geo.rs + kGroupRows * g + 32 * j + lane;
+      if (r >= geo.re) continue;
+      const int64_t b = static_cast<int64_t>(rp[r]), e = static_cast<int64_t>(rp[r + 1]);
+      if (e == b) continue;
+      // longest run of entries inside one tile (columns ascend)
+      int run = 0, worst = 0;
+      int64_t cur = -1;
+      for (int64_t i = b; i < e; ++i) {
+        const int64_t t = geo.tile(entry_col<KIND>(r, ci[i]));
+        run = t == cur ? run + 1 : 1;
+        cur = t;
+        worst = run > worst ? run : worst;
+      }
+      if (worst > 15) {
+        sk |= 1u << j;
+        ++ovf;
+        continue;
+      }
+      kept += static_cast<int>(e - b);
+      tmin = min(tmin, geo.tile(entry_col<KIND>(r, ci[b])));
+      tmax = max(tmax, geo.tile(entry_col<KIND>(r, ci[e - 1])));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+      tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+      kept += __shfl_xor_sync(0xffffffffu, kept, o);
+      ovf += __shfl_xor_sync(0xffffffffu, ovf, o);
+    }
+    skip[32 * g + lane] = static_cast<uint16_t>(sk);
+    if (lane == 0) {
+      const bool any = tmax >= 0;
+      nt_counts[g] = any ? static_cast<int32_t>(tmax - tmin + 1) : 0;
+      tile_lo[g] = any ? static_cast<int32_t>(tmin) : 0;
+      ent_counts[g] = kept;
+      ovf_counts[g] = ovf;
+    }
+  }
+}
+
+// IT / VB: raw element types of the inner / value widths (bit copies).
+template <int KIND, class RP, class CI, class IT, class VB>
+__global__ void __launch_bounds__(128) tiles_fill_kernel(
+    const RP* __restrict__ rp, const CI* __restrict__ ci, const VB* __restrict__ v,
+    TileGeom geo, int64_t ngroups, const int64_t* __restrict__ ent_ptr,
+    const int64_t* __restrict__ cnt_ptr, const int32_t* __restrict__ tile_lo,
+    const uint16_t* __restrict__ skip, const int64_t* __restrict__ ovf_ptr,
+    uint64_t* __restrict__ counts, IT* __restrict__ t_inner, VB* __restrict__ t_values,
+    int64_t* __restrict__ ovf_rows) {
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const IT* __restrict__ raw_ci = reinterpret_cast<const IT*>(ci);
+  for (int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < ngroups;
+       g += nw) {
+    const unsigned sk = skip[32 * g + lane];
+    // left-out rows, ascending (row order = j-major, lane-minor)
+    int64_t op = ovf_ptr[g];
+    for (int j = 0; j < kRowsPerLane; ++j) {
+      const bool o = (sk >> j) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, o);
+      if (o) ovf_rows[op + __popc(m & below)] = geo.rs + kGroupRows * g + 32 * j + lane;
+      op += __popc(m);
+    }
+    int64_t cur[kRowsPerLane], end[kRowsPerLane];
+#pragma unroll
+    for (int j = 0; j < kRowsPerLane; ++j) {
+      const int64_t r = geo.rs + kGroupRows * g + 32 * j + lane;
+      cur[j] = end[j] = 0;
+      if (r < geo.re && !((sk >> j) & 1u)) {
+        cur[j] = static_cast<int64_t>(rp[r]);
+        end[j] = static_cast<int64_t>(rp[r + 1]);
+      }
+    }
+    const int64_t nt = cnt_ptr[g + 1] - cnt_ptr[g];
+    const int64_t t0 = tile_lo[g];
+    int64_t pos = ent_ptr[g];
+    for (int64_t k = 0; k < nt; ++k) {
+      const int64_t t = t0 + k;
+      // this tile's entries of each row: [cur[j], cur[j] + n[j])
+      uint64_t nib = 0;
+      int total = 0;
+      int n[kRowsPerLane];
+#pragma unroll
+      for (int j = 0; j < kRowsPerLane; ++j) {
+        const int64_t r = geo.rs + kGroupRows * g + 32 * j + lane;
+        int c = 0;
+        while (cur[j] + c < end[j] && geo.tile(entry_col<KIND>(r, ci[cur[j] + c])) == t) ++c;
+        n[j] = c;
+        total += c;
+        nib |= static_cast<uint64_t>(c) << (4 * j);
+      }
+      counts[(cnt_ptr[g] + k) * 32 + lane] = nib;
+      const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
+      int j = 0, used = 0;
+      for (int s = 0; s < kmax; ++s) {
+        const bool act = s < total;
+        const unsigned m = __ballot_sync(0xffffffffu, act);
+        if (act) {
+          while (used == n[j]) {
+            ++j;
+            used = 0;
+          }
+          const int64_t src = cur[j] + used;
+          const int64_t dst = pos + __popc(m & below);
+          t_inner[dst] = raw_ci[src];
+          t_values[dst] = v[src];
+          ++used;
+        }
+        pos += __popc(m);
+      }
+#pragma unroll
+      for (int jj = 0; jj < kRowsPerLane; ++jj) cur[jj] += n[jj];
+    }
+  }
+}
+
+int grid_for_groups(int64_t ngroups, int warps_per_block) {
+  const int64_t blocks = (ngroups + warps_per_block - 1) / warps_per_block;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 64)));
+}
+
+const int kBytes[8] = {1, 2, 4, 8, 4, 8, 2, 2};
+
+template <int KIND, class RP, class CI, class F>
+int with_value_raw(const dacsr_matrix_t* a, F&& f) {
+  switch (kBytes[a->values_dtype]) {
+    case 8: return f(std::integral_constant<int, KIND>(), RP(), CI(), uint64_t());
+    case 4: return f(std::integral_constant<int, KIND>(), RP(), CI(), uint32_t());
+    case 2: return f(std::integral_constant<int, KIND>(), RP(), CI(), uint16_t());
+    default: return DACSR_ERR_DTYPE;
+  }
+}
+
+template <int KIND, class RP, class F>
+int with_inner(const dacsr_matrix_t* a, F&& f) {
+  if (KIND == DACSR_KIND_DA) {
+    switch (a->colids_dtype) {
+      case DACSR_I8: return with_value_raw<KIND, RP, int8_t>(a, f);
+      case DACSR_I16: return with_value_raw<KIND, RP, int16_t>(a, f);
+      case DACSR_I32: return with_value_raw<KIND, RP, int32_t>(a, f);
+      default: return DACSR_ERR_DTYPE;
+    }
+  }
+  switch (a->colids_dtype) {
+    case DACSR_I32: return with_value_raw<KIND, RP, int32_t>(a, f);
+    case DACSR_I64: return with_value_raw<KIND, RP, int64_t>(a, f);
+    default: return DACSR_ERR_DTYPE;
+  }
+}
+
+// f(kind_constant, RP(), CI(), VB()) for the matrix's types
+template <class F>
+int by_matrix_types(const dacsr_matrix_t* a, F&& f) {
+  if (a->values_dtype < DACSR_F32 || a->values_dtype > DACSR_BF16) return DACSR_ERR_DTYPE;
+  const bool i64 = a->rowptr_dtype == DACSR_I64;
+  if (!i64 && a->rowptr_dtype != DACSR_I32) return DACSR_ERR_DTYPE;
+  if (a->kind == DACSR_KIND_DA)
+    return i64 ? with_inner<DACSR_KIND_DA, int64_t>(a, f) : with_inner<DACSR_KIND_DA, int32_t>(a, f);
+  if (a->kind == DACSR_KIND_CSR)
+    return i64 ? with_inner<DACSR_KIND_CSR, int64_t>(a, f)
+               : with_inner<DACSR_KIND_CSR, int32_t>(a, f);
+  return DACSR_ERR_DTYPE;
+}
+
+template <class T>
+struct RawOf;
+template <> struct RawOf<int8_t> { using type = uint8_t; };
+template <> struct RawOf<int16_t> { using type = uint16_t; };
+template <> struct RawOf<int32_t> { using type = uint32_t; };
+template <> struct RawOf<int64_t> { using type = uint64_t; };
+
+bool geometry_ok(const dacsr_matrix_t* a, const dacsr_tiles_t* t) {
+  return a && t && a->rowptr && t->row_start >= 0 && t->row_end >= t->row_start &&
+         t->row_end <= a->nrows && t->ngroups == (t->row_end - t->row_start + 511) / 512 &&
+         t->tile_cols >= 64 && t->tile_cols <= 65536 && (t->tile_cols & 15) == 0 &&
+         (a->nnz == 0 || (a->colids && a->values));
+}
+
+}  // namespace
+}  // namespace dacsr
+
+using namespace dacsr;
+
+extern "C" {
+
+int dacsr_tiles_extent(const dacsr_matrix_t* a, int64_t rs, int64_t re, int64_t* out2, void* stream) {
+  if (!a || !a->rowptr || !out2 || rs < 0 || re < rs || re > a->nrows ||
+      (a->nnz > 0 && !a->colids))
+    return DACSR_ERR_ARG;
+  auto st = static_cast<cudaStream_t>(stream);
+  auto* o = reinterpret_cast<long long*>(out2);
+  extent_init_kernel<<<1, 1, 0, st>>>(o);
+  int rc = check_launch("extent_init_kernel");
+  if (rc || re == rs) return rc;
+  const int g = static_cast<int>(std::min<int64_t>((re - rs + 255) / 256, 148 * 16));
+  return by_matrix_types(a, [&](auto kc, auto rp0, auto ci0, auto) {
+    constexpr int KIND = decltype(kc)::value;
+    using RP = decltype(rp0);
+    using CI = decltype(ci0);
+    extent_kernel<KIND, RP, CI><<<g, 256, 0, st>>>(static_cast<const RP*>(a->rowptr),
+                                                   static_cast<const CI*>(a->colids), rs, re, o);
+    return check_launch("extent_kernel");
+  });
+}
+
+int dacsr_tiles_count(const dacsr_matrix_t* a, const dacsr_tiles_t* t, int32_t* nt_counts,
+                      int32_t* ent_counts, int32_t* ovf_counts, void* stream) {
+  if (!geometry_ok(a, t) || (t->ngroups > 0 && (!nt_counts || !ent_counts || !ovf_counts ||
+                                                !t->tile_lo || !t->skip)))
+    return DACSR_ERR_ARG;
+  if (t->ngroups == 0) return DACSR_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const TileGeom geo{t->row_start, t->row_end, t->col0, t->tile_cols};
+  const int g = grid_for_groups(t->ngroups, 8);
+  return by_matrix_types(a, [&](auto kc, auto rp0, auto ci0, auto) {
+    constexpr int KIND = decltype(kc)::value;
+    using RP = decltype(rp0);
+    using CI = decltype(ci0);
+    tiles_count_kernel<KIND, RP, CI><<<g, 256, 0, st>>>(
+        static_cast<const RP*>(a->rowptr), static_cast<const CI*>(a->colids), geo, t->ngroups,
+        nt_counts, ent_counts, ovf_counts, const_cast<int32_t*>(t->tile_lo),
+        const_cast<uint16_t*>(t->skip));
+    return check_launch("tiles_count_kernel");
+  });
+}
+
+int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int64_t* ovf_ptr,
+                     void* stream) {
+  if (!geometry_ok(a, t) || !ovf_ptr ||
+      (t->ngroups > 0 && (!t->ent_ptr || !t->cnt_ptr || !t->tile_lo || !t->skip)) ||
+      (t->nblocks > 0 && !t->counts) || (t->total > 0 && (!t->inner || !t->values)) ||
+      (t->n_ovf > 0 && !t->ovf_rows))
+    return DACSR_ERR_ARG;
+  if (t->ngroups == 0) return DACSR_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const TileGeom geo{t->row_start, t->row_end, t->col0, t->tile_cols};
+  const int g = grid_for_groups(t->ngroups, 4);
+  return by_matrix_types(a, [&](auto kc, auto rp0, auto ci0, auto vb0) {
+    constexpr int KIND = decltype(kc)::value;
+    using RP = decltype(rp0);
+    using CI = decltype(ci0);
+    using VB = decltype(vb0);
+    using IT = typename RawOf<CI>::type;
+    tiles_fill_kernel<KIND, RP, CI, IT, VB><<<g, 128, 0, st>>>(
+        static_cast<const RP*>(a->rowptr), static_cast<const CI*>(a->colids),
+        static_cast<const VB*>(a->values), geo, t->ngroups, t->ent_ptr, t->cnt_ptr, t->tile_lo,
+        t->skip, ovf_ptr, const_cast<uint64_t*>(t->counts),
+        static_cast<IT*>(const_cast<void*>(t->inner)), static_cast<VB*>(const_cast<void*>(t->values)),
+        const_cast<int64_t*>(t->ovf_rows));
+    return check_launch("tiles_fill_kernel");
+  });
+}
+
+}  // extern "C"

@@ -82,6 +82,7 @@ class DeviceMatrix:
         self._block_rows = None
         self._chunk_plans = {}
         self._sliced = None  # (plan, Slices, tensors) once build_slices ran
+        self._tiled = None   # (plan, Tiles, tensors) once build_tiles ran
         self._launch_cache = {}
         self._spmv_fn = _native.lib().dacsr_spmv
         self.tuned_kernel = None
@@ -307,13 +308,94 @@ class DeviceMatrix:
         plan = _native.Plan()
         ctypes.memmove(ctypes.byref(plan), ctypes.byref(self.plan), ctypes.sizeof(plan))
         plan.slices = ctypes.addressof(sl)
+        plan.tiles = self._tiled[0].tiles if self._tiled is not None else None
         plan.ctas_per_sm = getattr(self, "_ctas_per_sm", 0)
         tensors = {"row_len": row_len, "slice_ptr": ptrs[0], "inner": inner, "values": values,
                    "medium_rows": medium_rows, "m_slice_ptr": m_ptr, "m_inner": m_inner,
                    "m_values": m_values, "long_rows": long_rows}
         self._sliced = (plan, sl, tensors)
-        self._launch_cache.clear()
+        self._invalidate_launches()
         return plan
+
+    def build_tiles(self, tile_cols=None, stream=None):
+        """Build the band-tiled device layout (dacsr_tiles_t) of rows
+        [row_start, row_end) for the TILED kernel: 512-row groups, columns in
+        tiles of ``tile_cols`` (default 64 KiB of x values: 8192 for f64),
+        each group's entries stored tile by tile in the order its lanes fold
+        them.  A bit-for-bit copy of the entries (about the operator's size
+        again in HBM, plus half a byte per row and tile of counts).  Returns
+        the plan that carries it (variant "tiled")."""
+        L = _native.lib()
+        if self.plan is None:
+            self.build_plan(stream=stream)
+        if tile_cols is None:
+            tile_cols = 65536 // self.values.element_size()
+        tile_cols = int(tile_cols)
+        if tile_cols < 64 or tile_cols > 65536 or tile_cols % 16:
+            raise ValueError("tile_cols must be a multiple of 16 in [64, 65536]")
+        rs, re = self.row_start, self.row_end
+        dev = self.device
+        sp = _stream_ptr(stream)
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())
+        ng = (re - rs + 511) // 512
+        with torch.cuda.device(dev):
+            ext = torch.empty(2, dtype=torch.int64, device=dev)
+            _native.check(L.dacsr_tiles_extent(ctypes.byref(self.desc), rs, re, vp(ext), sp),
+                          "dacsr_tiles_extent")
+            cmin, cmax = (int(v) for v in ext.tolist())
+            if cmax < cmin:  # no entries
+                cmin = cmax = 0
+            tile_lo = torch.zeros(max(ng, 1), dtype=torch.int32, device=dev)
+            skip = torch.zeros(max(32 * ng, 1), dtype=torch.int16, device=dev)  # uint16 bits
+            tl = _native.Tiles(rs, re, ng, cmin, cmax, tile_cols, 0, 0, 0, None, None,
+                               tile_lo.data_ptr(), None, skip.data_ptr(), None, None, 0, None)
+            cnt = torch.zeros(3, max(ng, 1), dtype=torch.int32, device=dev)
+            _native.check(L.dacsr_tiles_count(ctypes.byref(self.desc), ctypes.byref(tl),
+                                               vp(cnt[0]), vp(cnt[1]), vp(cnt[2]), sp),
+                          "dacsr_tiles_count")
+            ptrs = torch.zeros(3, ng + 1, dtype=torch.int64, device=dev)
+            if ng:
+                for k in range(3):
+                    self._scan(cnt[k, :ng], ptrs[k, :ng + 1], sp)
+            nblocks, total, n_ovf = (int(v) for v in ptrs[:, ng].tolist())
+            counts = torch.empty(max(32 * nblocks, 1), dtype=torch.int64, device=dev)  # uint64 bits
+            inner = torch.zeros(total + 16, dtype=self.colids.dtype, device=dev)
+            values = torch.zeros(total + 16, dtype=self.values.dtype, device=dev)
+            ovf_rows = torch.empty(max(n_ovf, 1), dtype=torch.int64, device=dev)
+            tl.total, tl.nblocks, tl.n_ovf = total, nblocks, n_ovf
+            tl.cnt_ptr, tl.ent_ptr = ptrs[0].data_ptr(), ptrs[1].data_ptr()
+            tl.counts, tl.inner, tl.values = counts.data_ptr(), inner.data_ptr(), values.data_ptr()
+            tl.ovf_rows = ovf_rows.data_ptr()
+            _native.check(L.dacsr_tiles_fill(ctypes.byref(self.desc), ctypes.byref(tl),
+                                              vp(ptrs[2]), sp), "dacsr_tiles_fill")
+        plan = _native.Plan()
+        ctypes.memmove(ctypes.byref(plan), ctypes.byref(self.plan), ctypes.sizeof(plan))
+        plan.slices = self._sliced[0].slices if self._sliced is not None else None
+        plan.tiles = ctypes.addressof(tl)
+        tensors = {"ptrs": ptrs, "tile_lo": tile_lo, "skip": skip, "counts": counts,
+                   "inner": inner, "values": values, "ovf_rows": ovf_rows}
+        self._tiled = (plan, tl, tensors)
+        self._invalidate_launches()
+        return plan
+
+    def tiles_info(self):
+        """Summary of the band-tiled layout (None before build_tiles)."""
+        if self._tiled is None:
+            return None
+        _, tl, tensors = self._tiled
+        ng = max(1, tl.ngroups)
+        return {"tile_cols": tl.tile_cols, "col0": tl.col0, "cmax": tl.cmax,
+                "groups": tl.ngroups, "tile_blocks": tl.nblocks,
+                "tiles_per_group": tl.nblocks / ng, "entries": tl.total, "n_ovf": tl.n_ovf,
+                "count_bytes_per_row": 8 * tl.nblocks * 32 / max(1, tl.row_end - tl.row_start),
+                "bytes": sum(t.numel() * t.element_size() for t in tensors.values())}
+
+    def _invalidate_launches(self):
+        """Forget cached launch records and host-path plans (they hold raw
+        pointers into the layouts)."""
+        self._launch_cache.clear()
+        if getattr(self, "_streamed", None) is not None:
+            self._streamed._plans.clear()
 
     def slices_info(self):
         """Summary of the sliced layout (None before build_slices)."""
@@ -418,7 +500,7 @@ class DeviceMatrix:
         if self._sliced is not None:
             self._sliced[0].ctas_per_sm = int(n)
         self._ctas_per_sm = int(n)
-        self._launch_cache.clear()
+        self._invalidate_launches()
 
     def set_chunk_window(self, vcap, rows=None):
         """Pin the WSTREAM staging window (entries, multiple of 16) and the
@@ -437,6 +519,10 @@ class DeviceMatrix:
             if not (self.row_start <= rs <= re <= self.row_end):
                 return None
             return self._sliced[0] if self._sliced is not None else self.build_slices()
+        if kname == "tiled":
+            if not (self.row_start <= rs <= re <= self.row_end):
+                return None
+            return self._tiled[0] if self._tiled is not None else self.build_tiles()
         if self.plan is None or rs != self.plan.row_start or re != self.plan.row_end:
             return None
         if kname == "wstream":

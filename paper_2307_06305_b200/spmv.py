@@ -49,7 +49,7 @@ _EXACT = {
     "strip_mined_4": ("exact", _native.ORDER_STRIP4),
 }
 _EXACT_KERNELS = ("rowblock", "staged", "scalar", "wstream", "sliced", "sliced_tma",
-                  "sliced_ring", "sliced_pred", "sliced_pipe")
+                  "sliced_ring", "sliced_pred", "sliced_pipe", "tiled")
 _SLICED = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe")  # the sliced layout
 _TREE_KERNELS = ("vector2", "vector4", "vector8", "vector16", "warp")
 GPU_VARIANTS = ("auto", "rowblock_tree") + _EXACT_KERNELS + _TREE_KERNELS
@@ -130,9 +130,10 @@ def kernel_for(dm, kname, order):
         if dm.stats is None:
             return "staged"
         kname = _CODE_NAME[_native.lib().dacsr_select_variant(dm.stats, order)]
-    if kname in ("wstream",) + _SLICED and order in (_native.ORDER_MACC3, _native.ORDER_STRIP4):
-        kname = "rowblock"  # warp streams / slices specialise the naive order
-    if kname in ("rowblock", "wstream") + _SLICED and dm.plan is None:
+    if kname in ("wstream", "tiled") + _SLICED and order in (_native.ORDER_MACC3,
+                                                             _native.ORDER_STRIP4):
+        kname = "rowblock"  # warp streams / slices / tiles specialise the naive order
+    if kname in ("rowblock", "wstream", "tiled") + _SLICED and dm.plan is None:
         return "staged"
     return kname
 
