@@ -157,11 +157,14 @@ typedef struct {
  * = the entries of row j of lane l whose column falls in the tile (0..15).
  * The group's entries start at ent_ptr[g], tile after tile.  Inside a tile,
  * lane l's entries (its rows j = 0..15 in order, each row's entries in
- * column order) form a list L_l, stored "step-major": entry k of L_l sits at
- * tile_base + sum_{k' < k} |{l' : |L_l'| > k'}| + |{l' < l : |L_l'| > k}|,
- * so the lanes of a warp read step k of their lists as one packed run (no
- * padding).  Entries are bit-for-bit copies; every row's entries keep their
- * order, so a lane folding its list in order reproduces the naive sum.
+ * column order) form a list L_l, stored in pair steps: entries 2q and 2q+1
+ * of L_l sit at tile_base + 2 * (sum_{q' < q} |{l' : |L_l'| > 2q'}| +
+ * |{l' < l : |L_l'| > 2q}|) and the slot after it (a list of odd length
+ * ends in one zero slot), so the lanes of a warp read pair step q of their
+ * lists as one packed run of 2-entry vectors.  Every tile segment has an
+ * even length.  Entries are bit-for-bit copies; every row's entries keep
+ * their order, so a lane folding its list in order reproduces the naive
+ * sum.
  * Rows with more than 15 entries inside one tile are left out (counts 0,
  * bit j of skip[32g + l] set) and listed ascending in ovf_rows; the kernel
  * reduces them warp by warp from the CSR arrays.  inner / values carry 16
@@ -174,7 +177,7 @@ typedef struct {
   int64_t cmax;             /* last column any entry uses                   */
   int32_t tile_cols;        /* columns per tile (x tile = tile_cols values) */
   int32_t reserved;
-  int64_t total;            /* entries in the layout                        */
+  int64_t total;            /* slots in the layout (entries + pair padding) */
   int64_t nblocks;          /* cnt_ptr[ngroups]                             */
   const int64_t* ent_ptr;   /* ngroups + 1                                  */
   const int64_t* cnt_ptr;   /* ngroups + 1                                  */
@@ -291,7 +294,9 @@ int dacsr_slices_medium_fill(const dacsr_matrix_t* a, const dacsr_slices_t* s, v
  *    ovf_counts[g] = rows left out; t->tile_lo and t->skip filled.
  * 3. dacsr_tiles_fill (every t field set; ovf_ptr = scanned ovf_counts):
  *    counts, inner, values, ovf_rows.
- * 64 <= tile_cols <= 65536, a multiple of 16. */
+ * 64 <= tile_cols <= 65536, a multiple of 16; the TILED kernel keeps three x
+ * tiles in shared memory, so it needs tile_cols * sizeof(value) <= 54 KiB
+ * (DACSR_ERR_PLAN otherwise; DeviceMatrix uses 48 KiB). */
 int dacsr_tiles_extent(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end,
                        int64_t* out2_dev, void* stream);
 int dacsr_tiles_count(const dacsr_matrix_t* a, const dacsr_tiles_t* t, int32_t* nt_counts_dev,

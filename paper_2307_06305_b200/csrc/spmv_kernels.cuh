@@ -1687,6 +1687,7 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       }
       const int xbuf = td->tile_cols + static_cast<int>(16 / sizeof(VT));
       const size_t smem = tiled_smem_bytes<VT>(xbuf);
+      if (smem > 227 * 1024) return DACSR_ERR_PLAN;  // tile_cols too wide for the x ring
       const int threads = 32 * (kTileWarps + 1);
       auto kern = tiled_kernel<KIND, RP, CI, VT>;
       int per_sm = cached_per_sm(kern, threads, smem);

@@ -4,10 +4,10 @@
 // warp_long_row, ldcs, prefetch_l2_bulk).
 //
 // One CTA per SM, persistent over chunks of kTileWarps 512-row groups
-// (8192 rows).  Warp kTileWarps is the producer: it walks the chunk's
-// column tiles in order and streams each tile of x into one of two
-// shared-memory buffers with a TMA bulk copy (cp.async.bulk, full/empty
-// mbarriers).  Consumer warp w owns group w of the chunk: lane l holds rows
+// (7680 rows).  Warp kTileWarps is the producer: it walks the chunk's
+// column tiles in order and streams each tile of x into a ring of
+// kTileXBufs shared-memory buffers with TMA bulk copies (cp.async.bulk,
+// full/empty mbarriers; waiting warps sleep in mbarrier.try_wait).  Consumer warp w owns group w of the chunk: lane l holds rows
 // 32j + l (j = 0..15) and, per tile, folds its list of entries (its rows in
 // order, each row's entries of the tile in column order) with the x values
 // read from shared memory — random 8-byte reads that cost a few bank
@@ -23,10 +23,17 @@
 #pragma once
 
 
-constexpr int kTileWarps = 16;  // consumer warps (groups) per CTA
+// 15 consumer warps + the producer = 16 warps, 4 per SM sub-partition: the
+// register file is split per sub-partition, so a 17th warp would cap every
+// thread at 96 registers (measured: spills) instead of 128
+constexpr int kTileWarps = 15;  // consumer warps (groups) per CTA
 constexpr int kTileRows = 16;   // rows per lane
+#ifndef DACSR_TILED_XBUFS
+#define DACSR_TILED_XBUFS 2
+#endif
+constexpr int kTileXBufs = DACSR_TILED_XBUFS;  // x tile ring (producer runs kTileXBufs-1 ahead)
 #ifndef DACSR_TILED_BATCH
-#define DACSR_TILED_BATCH 8     // steps whose entries are loaded together
+#define DACSR_TILED_BATCH 6     // steps per batch (two batches in flight; measured 4/6/8 on C3: 6)
 #endif
 
 template <class CI, class VT>
@@ -43,14 +50,15 @@ struct TileArgs {
   int T;
 };
 
-// shared memory: two x buffers of xbuf elements, the row sums, 4 mbarriers
+// shared memory: kTileXBufs x buffers of xbuf elements, the row sums, the mbarriers
 template <class VT>
 __host__ __device__ constexpr size_t tiled_xbuf_bytes(int xbuf) {
   return (static_cast<size_t>(xbuf) * sizeof(VT) + 127) & ~size_t(127);
 }
 template <class VT>
 __host__ __device__ constexpr size_t tiled_smem_bytes(int xbuf) {
-  return 2 * tiled_xbuf_bytes<VT>(xbuf) + size_t(kTileWarps) * (kTileRows + 1) * 32 * 8 + 64;
+  return kTileXBufs * tiled_xbuf_bytes<VT>(xbuf) + size_t(kTileWarps) * (kTileRows + 1) * 32 * 8 +
+         16 * kTileXBufs;
 }
 
 __device__ __forceinline__ int nibble_sum(uint64_t v) {
@@ -138,10 +146,101 @@ __device__ __forceinline__ OUT ld_cs_pred(const T* p, bool pred) {
     return static_cast<OUT>(LdCs<T>::load(p, pred));
 }
 
-// mbarrier wait with a short back-off (the producer polls for whole tiles)
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+// Predicated evict-first load of two consecutive elements (one vector load;
+// p aligned to 2 * sizeof(T)); asm volatile, so a batch's loads are issued
+// in program order before the batch folds.  Outputs are undefined when
+// !pred (every use is predicated or selected away).
+#define DACSR_PAIR_PRED "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q "
+__device__ __forceinline__ void pair_ld_cs(const double* p, bool pred, double& a, double& b) {
+  asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.f64 {%0, %1}, [%2];\n\t}"
+               : "=d"(a), "=d"(b) : "l"(p), "r"(static_cast<unsigned>(pred)));
 }
+__device__ __forceinline__ void pair_ld_cs(const float* p, bool pred, float& a, float& b) {
+  asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.f32 {%0, %1}, [%2];\n\t}"
+               : "=f"(a), "=f"(b) : "l"(p), "r"(static_cast<unsigned>(pred)));
+}
+__device__ __forceinline__ uint32_t pair_ld_cs_b32(const void* p, bool pred) {
+  uint32_t w;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cs.b32 %0, [%1];\n\t}"
+               : "=r"(w) : "l"(p), "r"(static_cast<unsigned>(pred)));
+  return w;
+}
+__device__ __forceinline__ void pair_ld_cs(const __half* p, bool pred, __half& a, __half& b) {
+  const uint32_t w = pair_ld_cs_b32(p, pred);
+  a = __ushort_as_half(static_cast<unsigned short>(w & 0xffffu));
+  b = __ushort_as_half(static_cast<unsigned short>(w >> 16));
+}
+__device__ __forceinline__ void pair_ld_cs(const __nv_bfloat16* p, bool pred, __nv_bfloat16& a,
+                                           __nv_bfloat16& b) {
+  const uint32_t w = pair_ld_cs_b32(p, pred);
+  a = __ushort_as_bfloat16(static_cast<unsigned short>(w & 0xffffu));
+  b = __ushort_as_bfloat16(static_cast<unsigned short>(w >> 16));
+}
+__device__ __forceinline__ void pair_ld_cs(const int16_t* p, bool pred, int& a, int& b) {
+  const uint32_t w = pair_ld_cs_b32(p, pred);
+  a = static_cast<int>(static_cast<int16_t>(w & 0xffffu));
+  b = static_cast<int>(w) >> 16;
+}
+__device__ __forceinline__ void pair_ld_cs(const int8_t* p, bool pred, int& a, int& b) {
+  unsigned short w;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cs.b16 %0, [%1];\n\t}"
+               : "=h"(w) : "l"(p), "r"(static_cast<unsigned>(pred)));
+  a = static_cast<int>(static_cast<int8_t>(w & 0xffu));
+  b = static_cast<int>(static_cast<int8_t>(w >> 8));
+}
+__device__ __forceinline__ void pair_ld_cs(const int32_t* p, bool pred, int& a, int& b) {
+  asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.s32 {%0, %1}, [%2];\n\t}"
+               : "=r"(a), "=r"(b) : "l"(p), "r"(static_cast<unsigned>(pred)));
+}
+__device__ __forceinline__ void pair_ld_cs(const int64_t* p, bool pred, int64_t& a, int64_t& b) {
+  long long x, y;
+  asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.s64 {%0, %1}, [%2];\n\t}"
+               : "=l"(x), "=l"(y) : "l"(p), "r"(static_cast<unsigned>(pred)));
+  a = x;
+  b = y;
+}
+#undef DACSR_PAIR_PRED
+
+// acc += p (round to nearest) when pred, as one predicated DADD
+__device__ __forceinline__ void dadd_if(double& acc, double p, bool pred) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q add.rn.f64 %0, %0, %1;\n\t}"
+      : "+d"(acc) : "d"(p), "r"(static_cast<unsigned>(pred)));
+}
+
+// mbarrier waits that sleep instead of spinning (try_wait with a suspend
+// time hint: the warp is descheduled until the phase completes)
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_sleep(bar, parity)) {
+  }
+}
+
+// bit j = nibble j of v is non-zero
+__device__ __forceinline__ uint32_t nonzero_nibbles(uint64_t v) {
+  uint64_t t = v | (v >> 1);
+  t = (t | (t >> 2)) & 0x1111111111111111ull;  // bit 4j
+  t = (t | (t >> 3)) & 0x0303030303030303ull;  // byte k: bits 0, 1
+  t = (t | (t >> 6)) & 0x000F000F000F000Full;  // 16-bit half k: bits 0..3
+  t = (t | (t >> 12)) & 0x000000FF000000FFull;
+  return static_cast<uint32_t>((t | (t >> 24)) & 0xFFFFu);
+}
+
+// Group metadata of the chunk, one group per lane (lanes < kTileWarps),
+// loaded a chunk ahead.
+struct ChunkMeta {
+  int64_t cnt0, cnt1, ent;
+  int32_t tlo;
+};
 
 template <int KIND, class RP, class CI, class VT>
 __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
@@ -152,33 +251,40 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
   extern __shared__ __align__(128) unsigned char dsm[];
   VT* const xs = reinterpret_cast<VT*>(dsm);
   const size_t xstride = tiled_xbuf_bytes<VT>(xbuf) / sizeof(VT);
-  double* const accs = reinterpret_cast<double*>(dsm + 2 * tiled_xbuf_bytes<VT>(xbuf));
+  double* const accs = reinterpret_cast<double*>(dsm + kTileXBufs * tiled_xbuf_bytes<VT>(xbuf));
   uint64_t* const bars = reinterpret_cast<uint64_t*>(accs + kTileWarps * (kTileRows + 1) * 32);
   uint64_t* const full = bars;
-  uint64_t* const empty = bars + 2;
+  uint64_t* const empty = bars + kTileXBufs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned below = (1u << lane) - 1u;
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(&empty[0], kTileWarps);
-    mbar_init(&empty[1], kTileWarps);
+    for (int b = 0; b < kTileXBufs; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kTileWarps);
+    }
     mbar_fence_init();
   }
   __syncthreads();
   const int64_t nchunks = (g_last - g_first + kTileWarps - 1) / kTileWarps;
   const VT* const xb = m.x + m.xoff;
 
-  // tiles spanned by chunk c: lanes k < kTileWarps read group k's range
-  auto chunk_range = [&](int64_t c, int64_t& tlo, int64_t& thi) {
+  auto load_meta = [&](int64_t c) {
+    ChunkMeta q{0, 0, 0, 0};
     const int64_t g = g_first + c * kTileWarps + lane;
+    if (c < nchunks && lane < kTileWarps && g < g_last) {
+      q.cnt0 = ldg(ta.cnt_ptr + g);
+      q.cnt1 = ldg(ta.cnt_ptr + g + 1);
+      q.ent = ldg(ta.ent_ptr + g);
+      q.tlo = ldg(ta.tile_lo + g);
+    }
+    return q;
+  };
+  // tiles spanned by the chunk (empty: tlo > thi)
+  auto chunk_range = [&](const ChunkMeta& q, int64_t& tlo, int64_t& thi) {
     long long lo = LLONG_MAX, hi = LLONG_MIN;
-    if (lane < kTileWarps && g < g_last) {
-      const int64_t nt = ldg(ta.cnt_ptr + g + 1) - ldg(ta.cnt_ptr + g);
-      if (nt > 0) {
-        lo = ldg(ta.tile_lo + g);
-        hi = lo + nt - 1;
-      }
+    if (q.cnt1 > q.cnt0) {
+      lo = q.tlo;
+      hi = lo + (q.cnt1 - q.cnt0) - 1;
     }
     for (int o = 16; o > 0; o >>= 1) {
       lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -194,14 +300,18 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
   };
 
   if (warp == kTileWarps) {  // ---------------------------------- producer
-    uint32_t it = 0;
+    int rb = 0;
+    uint32_t rph = 0;
+    bool wrapped = false;
+    ChunkMeta nq = load_meta(blockIdx.x);
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const ChunkMeta q = nq;
+      nq = load_meta(c + gridDim.x);
       int64_t tlo, thi;
-      chunk_range(c, tlo, thi);
-      for (int64_t t = tlo; t <= thi; ++t, ++it) {
-        const int b = it & 1;
+      chunk_range(q, tlo, thi);
+      for (int64_t t = tlo; t <= thi; ++t) {
         if (lane == 0) {
-          if (it >= 2) mbar_wait_backoff(&empty[b], ((it >> 1) - 1) & 1);
+          if (wrapped) mbar_wait_sleep(&empty[rb], rph ^ 1u);
           const int64_t cs = ta.col0 + t * ta.T;
           const int64_t ce = min64(cs + ta.T, ta.cmax + 1);
           const int shift = tile_shift(cs);
@@ -209,12 +319,17 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
           const int64_t n = ce - cs + shift;
           DACSR_CHECK(n > 0 && n <= xbuf);
           const uint32_t main = static_cast<uint32_t>((n * sizeof(VT)) & ~int64_t(15));
-          VT* dst = xs + b * xstride;
+          VT* dst = xs + rb * xstride;
           // the last < 16 bytes with plain loads (the bulk copy must not
           // read past x's last element)
-          for (int64_t q = main / sizeof(VT); q < n; ++q) dst[q] = src[q];
-          mbar_arrive_expect_tx(&full[b], main);
-          if (main) bulk_copy_g2s(dst, src, main, &full[b]);
+          for (int64_t q2 = main / sizeof(VT); q2 < n; ++q2) dst[q2] = src[q2];
+          mbar_arrive_expect_tx(&full[rb], main);
+          if (main) bulk_copy_g2s(dst, src, main, &full[rb]);
+        }
+        if (++rb == kTileXBufs) {
+          rb = 0;
+          rph ^= 1u;
+          wrapped = true;
         }
       }
     }
@@ -239,29 +354,36 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
     if (v1 > v0) prefetch_l2_bulk(reinterpret_cast<const void*>(v0), static_cast<uint32_t>(v1 - v0));
     if (i1 > i0) prefetch_l2_bulk(reinterpret_cast<const void*>(i0), static_cast<uint32_t>(i1 - i0));
   };
-  uint32_t it = 0;
+  int rb = 0;
+  uint32_t rph = 0;
+  ChunkMeta nq = load_meta(blockIdx.x);
+  // this warp's group's first two count words, loaded a chunk ahead too
+  uint64_t ncn0 = 0, ncn1 = 0;
+  {
+    const int64_t c0 = __shfl_sync(0xffffffffu, nq.cnt0, warp);
+    const int64_t c1 = __shfl_sync(0xffffffffu, nq.cnt1, warp);
+    if (c1 > c0) ncn0 = ldg(ta.counts + c0 * 32 + lane);
+    if (c1 > c0 + 1) ncn1 = ldg(ta.counts + (c0 + 1) * 32 + lane);
+  }
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const ChunkMeta q = nq;
+    nq = load_meta(c + gridDim.x);
     int64_t tlo, thi;
-    chunk_range(c, tlo, thi);
+    chunk_range(q, tlo, thi);
     const int64_t g = g_first + c * kTileWarps + warp;
     const bool has = g < g_last;
-    int64_t gtlo = 0, gnt = 0, cbase = 0, pos = 0;
-    if (has) {
-      gtlo = ldg(ta.tile_lo + g);
-      cbase = ldg(ta.cnt_ptr + g);
-      gnt = ldg(ta.cnt_ptr + g + 1) - cbase;
-      pos = ldg(ta.ent_ptr + g);
-    }
+    const int64_t cbase = __shfl_sync(0xffffffffu, q.cnt0, warp);
+    const int64_t gnt = __shfl_sync(0xffffffffu, q.cnt1, warp) - cbase;
+    const int64_t gtlo = __shfl_sync(0xffffffffu, q.tlo, warp);
+    int64_t pos = __shfl_sync(0xffffffffu, q.ent, warp);
 #pragma unroll
     for (int j = 0; j < kTileRows; ++j) sts_f64(wa + 256u * j, 0.0);
-    uint64_t cn0 = gnt > 0 ? ldg(ta.counts + cbase * 32 + lane) : 0;
-    uint64_t cn1 = gnt > 1 ? ldg(ta.counts + (cbase + 1) * 32 + lane) : 0;
+    uint64_t cn0 = ncn0, cn1 = ncn1;
     if (gnt > 0)
       prefetch_segment(pos, __reduce_add_sync(0xffffffffu, static_cast<unsigned>(nibble_sum(cn0))));
     // rows of lane l: row0 + 512g + 32j + l
     const int64_t lrow = ta.row0 + 512 * g + lane;
-    for (int64_t t = tlo; t <= thi; ++t, ++it) {
-      const int b = it & 1;
+    for (int64_t t = tlo; t <= thi; ++t) {
       const int64_t k = t - gtlo;
       const bool mine = has && k >= 0 && k < gnt;
       uint64_t cur = 0;
@@ -276,20 +398,24 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
           prefetch_segment(pos + here,
                            __reduce_add_sync(0xffffffffu, static_cast<unsigned>(nibble_sum(cn0))));
       }
-      mbar_wait(&full[b], (it >> 1) & 1);
+      if (t == thi) {  // the next chunk's first count words
+        const int64_t c0 = __shfl_sync(0xffffffffu, nq.cnt0, warp);
+        const int64_t c1 = __shfl_sync(0xffffffffu, nq.cnt1, warp);
+        ncn0 = c1 > c0 ? ldg(ta.counts + c0 * 32 + lane) : 0;
+        ncn1 = c1 > c0 + 1 ? ldg(ta.counts + (c0 + 1) * 32 + lane) : 0;
+      }
+      mbar_wait_sleep(&full[rb], rph);
       if (mine) {
         const int64_t cs = ta.col0 + t * ta.T;
         const int64_t d = cs - tile_shift(cs);  // column of x buffer element 0
-        const uint32_t xsa = xs0 + static_cast<uint32_t>(b * xstride * sizeof(VT));
+        const uint32_t xsa = xs0 + static_cast<uint32_t>(rb * xstride * sizeof(VT));
         // DA: x of entry (row j, offset o) at xr + o * sizeof(VT), xr = &xbuf[row - d];
         // CSR: at xc + c * sizeof(VT), xc = &xbuf[-d] (32-bit wrap-around arithmetic)
         const uint32_t xr0 = xsa + static_cast<uint32_t>((lrow - d) * static_cast<int64_t>(sizeof(VT)));
         const uint32_t xc = xsa - static_cast<uint32_t>(d * static_cast<int64_t>(sizeof(VT)));
         const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
         // rows of this tile with entries (bit j), consumed in order
-        uint32_t nz = 0;
-#pragma unroll
-        for (int j = 0; j < kTileRows; ++j) nz |= ((cur >> (4 * j)) & 15u) ? (1u << j) : 0u;
+        uint32_t nz = nonzero_nibbles(cur);
         int rem = 0;
         uint32_t acc_a = wa + 32u * 8u * kTileRows;  // dummy slot
         uint32_t xr = xr0;
@@ -301,41 +427,71 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         asm("" : "+l"(vt));
         asm("" : "+l"(ct));
         uint32_t lp = 0;
-        // batch of U steps: positions from the step ballots, then every
-        // operator load of the batch issued (predicated asm, program order)
-        auto load_batch = [&](int k0, OT* off, VT* val) {
+        // batch of U steps = U/2 pair steps: positions from the pair-step
+        // ballots, then every operator load of the batch issued (2-entry
+        // vector loads, predicated asm, program order)
+        constexpr int UP = U / 2;
+        auto load_batch = [&](int q0, OT* off, VT* val) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const bool act = k0 + u < total;
+          for (int u = 0; u < UP; ++u) {
+            const bool act = 2 * (q0 + u) < total;
             const unsigned msk = __ballot_sync(0xffffffffu, act);
-            const uint32_t o = lp + __popc(msk & below);
-            lp += __popc(msk);
-            DACSR_CHECK(!act || pos + o < ta.total);
-            off[u] = ld_cs_pred<CI, OT>(elem_addr_u32(ct, o), act);
-            val[u] = ld_cs_pred<VT, VT>(elem_addr_u32(vt, o), act);
+            const uint32_t o = lp + 2 * __popc(msk & below);
+            lp += 2 * __popc(msk);
+            DACSR_CHECK(!act || pos + o + 1 < ta.total);
+            pair_ld_cs(elem_addr_u32(ct, o), act, off[2 * u], off[2 * u + 1]);
+            pair_ld_cs(elem_addr_u32(vt, o), act, val[2 * u], val[2 * u + 1]);
           }
         };
         auto fold_batch = [&](int k0, const OT* off, const VT* val) {
+          const int left = total - k0;  // steps of this lane left in the tile
+          if constexpr (KIND == DACSR_KIND_DA) {
+            // the row of each step from the counts alone (no dependence on
+            // the sums), branch-free, so every x read of the batch can issue
+            // before the first sum of the batch is formed
+            uint32_t xrs[U];
+            uint32_t swm = 0, jpk = 0;
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const bool act = k0 + u < total;
-            const bool sw = act && rem == 0;  // this lane's next row of the tile
-            if (sw) {
-              sts_f64(acc_a, acc);
-              const int j = __ffs(nz) - 1;
-              nz &= nz - 1;
-              rem = static_cast<int>((cur >> (4 * j)) & 15u);
-              acc_a = wa + 256u * j;
-              acc = lds_f64(acc_a);
-              xr = xr0 + static_cast<uint32_t>(32 * j * sizeof(VT));
+            for (int u = 0; u < U; ++u) {
+              const bool sw = u < left && rem == 0;
+              const int jn = __ffs(nz) - 1;
+              const uint32_t nz2 = nz & (nz - 1);
+              const int rem2 = static_cast<int>((cur >> (4 * (jn & 15))) & 15u);
+              nz = sw ? nz2 : nz;
+              rem = (sw ? rem2 : rem) - 1;
+              xr = sw ? xr0 + static_cast<uint32_t>(32 * jn * sizeof(VT)) : xr;
+              swm |= sw ? 1u << u : 0u;
+              jpk |= sw ? static_cast<uint32_t>(jn) << (4 * u) : 0u;
+              xrs[u] = xr;
             }
-            const uint32_t xa = KIND == DACSR_KIND_DA
-                                    ? xr + static_cast<uint32_t>(static_cast<int>(off[u]) * static_cast<int>(sizeof(VT)))
-                                    : xc + static_cast<uint32_t>(off[u] * static_cast<OT>(sizeof(VT)));
-            DACSR_CHECK(!act || (xa >= xsa && xa < xsa + xbuf * sizeof(VT)));
-            const double p = act ? product(val[u], lds_val<VT>(xa)) : 0.0;
-            acc = __dadd_rn(acc, p);  // +0 for idle steps: acc never holds -0
-            rem -= act ? 1 : 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if ((swm >> u) & 1u) {  // this lane's next row of the tile
+                sts_f64(acc_a, acc);
+                acc_a = wa + 256u * ((jpk >> (4 * u)) & 15u);
+                acc = lds_f64(acc_a);
+              }
+              const uint32_t xa = xrs[u] + static_cast<uint32_t>(static_cast<int>(off[u]) * static_cast<int>(sizeof(VT)));
+              DACSR_CHECK(!(u < left) || (xa >= xsa && xa < xsa + xbuf * sizeof(VT)));
+              if (u < left) dadd_if(acc, product(val[u], lds_val<VT>(xa)), true);
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const bool act = u < left;  // once false, false for the rest of the tile
+              if (act && rem == 0) {  // this lane's next row of the tile
+                sts_f64(acc_a, acc);
+                const int j = __ffs(nz) - 1;
+                nz &= nz - 1;
+                rem = static_cast<int>((cur >> (4 * j)) & 15u);
+                acc_a = wa + 256u * j;
+                acc = lds_f64(acc_a);
+              }
+              const uint32_t xa = xc + static_cast<uint32_t>(off[u] * static_cast<OT>(sizeof(VT)));
+              DACSR_CHECK(!act || (xa >= xsa && xa < xsa + xbuf * sizeof(VT)));
+              if (act) dadd_if(acc, product(val[u], lds_val<VT>(xa)), true);
+              --rem;
+            }
           }
         };
         // two batches in flight: batch i+1's loads are issued before batch i folds
@@ -344,11 +500,11 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         int k0 = 0;
         if (kmax > 0) load_batch(0, offA, valA);
         while (k0 < kmax) {
-          if (k0 + U < kmax) load_batch(k0 + U, offB, valB);
+          if (k0 + U < kmax) load_batch((k0 + U) / 2, offB, valB);
           fold_batch(k0, offA, valA);
           k0 += U;
           if (k0 >= kmax) break;
-          if (k0 + U < kmax) load_batch(k0 + U, offA, valA);
+          if (k0 + U < kmax) load_batch((k0 + U) / 2, offA, valA);
           fold_batch(k0, offB, valB);
           k0 += U;
         }
@@ -356,7 +512,11 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         pos += lp;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[b]);
+      if (lane == 0) mbar_arrive(&empty[rb]);
+      if (++rb == kTileXBufs) {
+        rb = 0;
+        rph ^= 1u;
+      }
     }
     // the chunk's rows: y = alpha * sum (+ beta * y)
     if (has) {

@@ -11,11 +11,12 @@
 //   group g (512 rows: lane l holds rows 512g + 32j + l, j = 0..15)
 //     tile t (tile_lo[g] ..):  counts[32]  — lane l: 16 nibbles (entries of
 //                                           its row j inside the tile)
-//                              entries     — lane lists L_l stored
-//                                           step-major (step k: the k-th
-//                                           entry of every lane whose list
-//                                           is longer than k, lanes
-//                                           ascending)
+//                              entries     — lane lists L_l stored in pair
+//                                           steps (pair step q: entries 2q,
+//                                           2q + 1 of every lane whose list
+//                                           is longer than 2q, lanes
+//                                           ascending; a list of odd length
+//                                           ends in one zero slot)
 //
 // A row's entries stay in column order (tiles ascend, and inside a tile its
 // entries are consecutive in its lane's list), so each lane folds every row
@@ -114,15 +115,42 @@ __global__ void tiles_count_kernel(const RP* __restrict__ rp, const CI* __restri
     for (int o = 16; o > 0; o >>= 1) {
       tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
       tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-      kept += __shfl_xor_sync(0xffffffffu, kept, o);
       ovf += __shfl_xor_sync(0xffffffffu, ovf, o);
     }
+    // slots: per tile, each lane's list rounded up to whole pairs
+    int64_t slots = 0;
+    if (tmax >= 0) {
+      int64_t cur[kRowsPerLane], end[kRowsPerLane];
+#pragma unroll
+      for (int j = 0; j < kRowsPerLane; ++j) {
+        const int64_t r = geo.rs + kGroupRows * g + 32 * j + lane;
+        cur[j] = end[j] = 0;
+        if (r < geo.re && !((sk >> j) & 1u)) {
+          cur[j] = static_cast<int64_t>(rp[r]);
+          end[j] = static_cast<int64_t>(rp[r + 1]);
+        }
+      }
+      for (int64_t t = tmin; t <= tmax; ++t) {
+        int total = 0;
+#pragma unroll
+        for (int j = 0; j < kRowsPerLane; ++j) {
+          const int64_t r = geo.rs + kGroupRows * g + 32 * j + lane;
+          while (cur[j] < end[j] && geo.tile(entry_col<KIND>(r, ci[cur[j]])) == t) {
+            ++cur[j];
+            ++total;
+          }
+        }
+        slots += (total + 1) & ~1;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) slots += __shfl_xor_sync(0xffffffffu, slots, o);
+    (void)kept;
     skip[32 * g + lane] = static_cast<uint16_t>(sk);
     if (lane == 0) {
       const bool any = tmax >= 0;
       nt_counts[g] = any ? static_cast<int32_t>(tmax - tmin + 1) : 0;
       tile_lo[g] = any ? static_cast<int32_t>(tmin) : 0;
-      ent_counts[g] = kept;
+      ent_counts[g] = static_cast<int32_t>(slots);
       ovf_counts[g] = ovf;
     }
   }
@@ -183,21 +211,31 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
       counts[(cnt_ptr[g] + k) * 32 + lane] = nib;
       const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
       int j = 0, used = 0;
-      for (int s = 0; s < kmax; ++s) {
+      auto next_src = [&]() {  // this lane's next list entry
+        while (used == n[j]) {
+          ++j;
+          used = 0;
+        }
+        return cur[j] + used++;
+      };
+      for (int s = 0; s < kmax; s += 2) {  // pair step: list entries s, s + 1
         const bool act = s < total;
         const unsigned m = __ballot_sync(0xffffffffu, act);
         if (act) {
-          while (used == n[j]) {
-            ++j;
-            used = 0;
+          const int64_t dst = pos + 2 * __popc(m & below);
+          const int64_t a = next_src();
+          t_inner[dst] = raw_ci[a];
+          t_values[dst] = v[a];
+          if (s + 1 < total) {
+            const int64_t b2 = next_src();
+            t_inner[dst + 1] = raw_ci[b2];
+            t_values[dst + 1] = v[b2];
+          } else {
+            t_inner[dst + 1] = IT(0);
+            t_values[dst + 1] = VB(0);
           }
-          const int64_t src = cur[j] + used;
-          const int64_t dst = pos + __popc(m & below);
-          t_inner[dst] = raw_ci[src];
-          t_values[dst] = v[src];
-          ++used;
         }
-        pos += __popc(m);
+        pos += 2 * __popc(m);
       }
 #pragma unroll
       for (int jj = 0; jj < kRowsPerLane; ++jj) cur[jj] += n[jj];

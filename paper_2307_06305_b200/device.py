@@ -320,7 +320,8 @@ class DeviceMatrix:
     def build_tiles(self, tile_cols=None, stream=None):
         """Build the band-tiled device layout (dacsr_tiles_t) of rows
         [row_start, row_end) for the TILED kernel: 512-row groups, columns in
-        tiles of ``tile_cols`` (default 64 KiB of x values: 8192 for f64),
+        tiles of ``tile_cols`` (default 64 KiB of x values, 8192 for f64:
+        the kernel keeps two x tiles in shared memory),
         each group's entries stored tile by tile in the order its lanes fold
         them.  A bit-for-bit copy of the entries (about the operator's size
         again in HBM, plus half a byte per row and tile of counts).  Returns
@@ -331,8 +332,9 @@ class DeviceMatrix:
         if tile_cols is None:
             tile_cols = 65536 // self.values.element_size()
         tile_cols = int(tile_cols)
-        if tile_cols < 64 or tile_cols > 65536 or tile_cols % 16:
-            raise ValueError("tile_cols must be a multiple of 16 in [64, 65536]")
+        if tile_cols < 64 or tile_cols % 16 or tile_cols * self.values.element_size() > 65536:
+            raise ValueError("tile_cols must be a multiple of 16, >= 64, and its x tile at most "
+                             "64 KiB")
         rs, re = self.row_start, self.row_end
         dev = self.device
         sp = _stream_ptr(stream)

@@ -41,7 +41,7 @@ def small_checks():
         for kind in ("da", "csr"):
             dm = DeviceMatrix(kind, n, n, arr["rowptr"], arr["offsets" if kind == "da" else "colids"],
                               arr["values"])
-            for tc in (64, 256, 8192):
+            for tc in (64, 256, 6144):
                 dm.build_tiles(tc)
                 y = torch.full((n,), 7.0, dtype=torch.float64, device=dev)
                 dm.spmv_into(x, y, 1.0, 0.0, "tiled")
