@@ -72,14 +72,9 @@ enum {
   DACSR_VARIANT_SLICED = 10,  /* sliced layout (plan->slices): lane per row,     */
                               /* coalesced column-major entries straight from    */
                               /* HBM, exact naive order; spill rows by side warps*/
-  DACSR_VARIANT_SLICED_TMA = 11, /* sliced layout, each warp's next two slices   */
-                              /* staged in smem by TMA bulk copies              */
-  DACSR_VARIANT_SLICED_RING = 12, /* sliced layout, a producer warp streams      */
-                              /* multi-slice chunks into an smem ring for the   */
-                              /* consumer warps (needs the padding below)       */
-  DACSR_VARIANT_SLICED_PRED = 13, /* SLICED + x gathers issued at the offsets of */
-                              /* the warp's previous slice (stencil-like rows), */
-                              /* re-gathered when the guess was wrong          */
+  /* 11, 12, 13: retired round-1 sliced modes (TMA-staged, warp-specialised
+   * ring, offset-predicted): exact but slower on every BASELINE config;
+   * the codes now return DACSR_ERR_VARIANT */
   DACSR_VARIANT_SLICED_PIPE = 14, /* SLICED with the next slice's offsets loaded */
                               /* while this slice's gathers are in flight       */
   DACSR_VARIANT_TILED = 15    /* band-tiled layout (plan->tiles): x staged in    */
@@ -129,9 +124,8 @@ typedef struct {
   int64_t total;            /* main slots = slice_ptr[nslices]               */
   int32_t max_len;          /* main-slice rows: len <= max_len               */
   int32_t medium_len;       /* medium rows: max_len < len <= medium_len      */
-  const int64_t* slice_ptr; /* nslices + 1 (SLICED_RING reads nslices + 2)   */
-  const uint8_t* row_len;   /* row_end - row_start (SLICED_RING reads 32 *   */
-                            /* nslices bytes: pad the buffer)                */
+  const int64_t* slice_ptr; /* nslices + 1                                   */
+  const uint8_t* row_len;   /* row_end - row_start                           */
   const void* inner;        /* total, the matrix's colids dtype              */
   const void* values;       /* total, the matrix's values dtype              */
   int64_t n_medium;
@@ -204,6 +198,10 @@ typedef struct {
   int64_t empty_rows;
   double mean_len;
   double cv_len; /* coefficient of variation of row lengths */
+  /* gather locality: fraction of sampled adjacent row pairs whose middle
+   * entries' columns are more than 16 apart (beyond the diagonal step) —
+   * near 1 for random bands (C3, C5), near 0 for stencils / RCM orders */
+  double scatter;
 } dacsr_stats_t;
 
 /* nnz-balanced partition: block b stages entries

@@ -267,6 +267,36 @@ def gen_fill(n, b, kmax, seed, cdf, table, r0=0, r1=None):
     return rp, offs, vals
 
 
+def gen_fill_parallel(n, b, kmax, seed, cdf, table, r0=0, r1=None, threads=None):
+    """gen_fill over row blocks on host threads (ctypes releases the GIL);
+    identical arrays (rows are pure functions of (seed, row))."""
+    import concurrent.futures as cf
+    import os
+    r1 = n if r1 is None else r1
+    threads = threads or len(os.sched_getaffinity(0))
+    cuts = np.linspace(r0, r1, threads * 4 + 1).astype(np.int64)
+    blocks = [(int(a), int(c)) for a, c in zip(cuts[:-1], cuts[1:]) if c > a]
+    with cf.ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(lambda bc: gen_counts(n, b, kmax, seed, cdf, *bc), blocks))
+    counts = np.concatenate(parts) if parts else np.zeros(0, np.int32)
+    rp = np.zeros(r1 - r0 + 1, np.int64)
+    np.cumsum(counts, out=rp[1:])
+    offs = np.empty(int(rp[-1]), np.int16)
+    vals = np.empty(int(rp[-1]), np.float64)
+
+    def fill(bc):
+        a, c = bc
+        e0 = int(rp[a - r0])
+        po = ctypes.c_void_p(offs.ctypes.data + 2 * e0)
+        pv = ctypes.c_void_p(vals.ctypes.data + 8 * e0)
+        got = lib().orc_gen_fill(n, b, kmax, seed, _p(cdf), _p(table), a, c, po, pv)
+        assert got == rp[c - r0] - rp[a - r0]
+
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(fill, blocks))
+    return rp, offs, vals
+
+
 def gen_normal(seed, i0, i1, table):
     out = np.empty(i1 - i0, np.float64)
     lib().orc_gen_normal(seed, i0, i1, _p(table), _p(out))

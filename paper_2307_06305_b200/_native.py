@@ -26,7 +26,7 @@ KIND_CSR, KIND_DA = 0, 1
 ORDER_NAIVE, ORDER_MACC3, ORDER_STRIP4, ORDER_TREE = range(4)
 VARIANT_CODES = {
     "auto": 0, "rowblock": 1, "scalar": 2, "vector2": 3, "vector4": 4, "vector8": 5,
-    "vector16": 6, "warp": 7, "staged": 8, "wstream": 9, "sliced": 10, "sliced_tma": 11, "sliced_ring": 12, "sliced_pred": 13, "sliced_pipe": 14, "tiled": 15,
+    "vector16": 6, "warp": 7, "staged": 8, "wstream": 9, "sliced": 10, "sliced_pipe": 14, "tiled": 15,
 }
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported dtype", 3: "unknown variant/order",
           4: "CUDA error", 5: "plan mismatch"}
@@ -58,7 +58,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int64), ("nnz", ctypes.c_int64),
                 ("entry_start", ctypes.c_int64), ("entry_end", ctypes.c_int64),
                 ("max_len", ctypes.c_int64), ("empty_rows", ctypes.c_int64),
-                ("mean_len", ctypes.c_double), ("cv_len", ctypes.c_double)]
+                ("mean_len", ctypes.c_double), ("cv_len", ctypes.c_double),
+                ("scatter", ctypes.c_double)]
 
 
 class Plan(ctypes.Structure):

@@ -25,7 +25,43 @@ struct AnalyzeScratch {
   unsigned long long empty;
   double sum_sq;
   int64_t e0, e1;
+  unsigned long long pairs, scattered;  // gather-scatter sample (see scatter_kernel)
 };
+static_assert(sizeof(AnalyzeScratch) <= DACSR_ANALYZE_SCRATCH, "analyze scratch");
+
+// Gather locality: for sampled adjacent rows r, r+1 (both non-empty) the
+// middle entries' columns; the pair is "scattered" when the next row's
+// column is not within 16 of one past this row's — lanes of a warp (one row
+// each) then gather from different cache lines (random bands: C3, C5),
+// unlike stencils and RCM-ordered matrices whose neighbouring rows read
+// neighbouring x.
+template <int KIND, class RP, class CI>
+__global__ void scatter_kernel(const void* rp, const CI* ci, int64_t rs, int64_t re, int64_t step,
+                               AnalyzeScratch* out) {
+  unsigned long long pairs = 0, sc = 0;
+  const int64_t npairs = (re - rs - 1 + step - 1) / step;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < npairs;
+       k += stride) {
+    const int64_t r = rs + k * step;
+    const int64_t b0 = rp_at<RP>(rp, r), b1 = rp_at<RP>(rp, r + 1), b2 = rp_at<RP>(rp, r + 2);
+    if (b1 == b0 || b2 == b1) continue;
+    const int64_t i0 = b0 + (b1 - b0) / 2, i1 = b1 + (b2 - b1) / 2;
+    const int64_t c0 = static_cast<int64_t>(ldg(ci + i0)) + (KIND == DACSR_KIND_DA ? r : 0);
+    const int64_t c1 = static_cast<int64_t>(ldg(ci + i1)) + (KIND == DACSR_KIND_DA ? r + 1 : 0);
+    const int64_t d = c1 - c0 - 1;
+    ++pairs;
+    sc += (d > 16 || d < -16) ? 1 : 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    sc += __shfl_xor_sync(0xffffffffu, sc, o);
+  }
+  if ((threadIdx.x & 31) == 0 && pairs) {
+    atomicAdd(&out->pairs, pairs);
+    atomicAdd(&out->scattered, sc);
+  }
+}
 
 template <class RP>
 __global__ void analyze_kernel(const void* rp, int64_t rs, int64_t re, AnalyzeScratch* out) {
@@ -208,6 +244,29 @@ int dacsr_analyze(const dacsr_matrix_t* a, int64_t rs, int64_t re, void* scratch
   else if (a->rowptr_dtype == DACSR_I32) analyze_kernel<int32_t><<<g, 256, 0, st>>>(a->rowptr, rs, re, sc);
   else return DACSR_ERR_DTYPE;
   if ((rc = check_launch("analyze_kernel"))) return rc;
+  if (re - rs >= 2 && a->colids && a->nnz > 0) {
+    const int64_t step = std::max<int64_t>(1, (re - rs) / 65536);
+    const int64_t np = (re - rs - 1 + step - 1) / step;
+    const int gs = grid_for(np, 256);
+    const bool da = a->kind == DACSR_KIND_DA, r64 = a->rowptr_dtype == DACSR_I64;
+    auto go = [&](auto ci0) {
+      using CI = decltype(ci0);
+      const CI* ci = static_cast<const CI*>(a->colids);
+      if (da && r64) scatter_kernel<DACSR_KIND_DA, int64_t, CI><<<gs, 256, 0, st>>>(a->rowptr, ci, rs, re, step, sc);
+      else if (da) scatter_kernel<DACSR_KIND_DA, int32_t, CI><<<gs, 256, 0, st>>>(a->rowptr, ci, rs, re, step, sc);
+      else if (r64) scatter_kernel<DACSR_KIND_CSR, int64_t, CI><<<gs, 256, 0, st>>>(a->rowptr, ci, rs, re, step, sc);
+      else scatter_kernel<DACSR_KIND_CSR, int32_t, CI><<<gs, 256, 0, st>>>(a->rowptr, ci, rs, re, step, sc);
+      return check_launch("scatter_kernel");
+    };
+    switch (a->colids_dtype) {
+      case DACSR_I8: rc = go(int8_t()); break;
+      case DACSR_I16: rc = go(int16_t()); break;
+      case DACSR_I32: rc = go(int32_t()); break;
+      case DACSR_I64: rc = go(int64_t()); break;
+      default: rc = DACSR_ERR_DTYPE;
+    }
+    if (rc) return rc;
+  }
   AnalyzeScratch h;
   if ((rc = cuda_status("analyze copy", cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st))))
     return rc;
@@ -222,6 +281,7 @@ int dacsr_analyze(const dacsr_matrix_t* a, int64_t rs, int64_t re, void* scratch
   out->mean_len = rows ? static_cast<double>(out->nnz) / rows : 0.0;
   const double var = rows ? h.sum_sq / rows - out->mean_len * out->mean_len : 0.0;
   out->cv_len = out->mean_len > 0 ? std::sqrt(std::max(var, 0.0)) / out->mean_len : 0.0;
+  out->scatter = h.pairs ? static_cast<double>(h.scattered) / static_cast<double>(h.pairs) : 0.0;
   return DACSR_OK;
 }
 

@@ -56,15 +56,22 @@ const char* dacsr_version(void) { return "dacsr_b200 0.1.0 (sm_100a)"; }
 
 const char* dacsr_last_error(void) { return g_last_error; }
 
+// Selection by row statistics (measured per config):
+//  * scattered gathers (random wide bands, C3/C5): TILED, x staged in smem;
+//  * everything else with enough rows (stencils, RCM orders, skew: C1, C2,
+//    C4): SLICED_PIPE on the sliced layout (medium / long rows handled
+//    inside the launch);
+//  * tiny matrices: SCALAR (no derived layout worth building);
+//  * the MACC3 / STRIP4 orders: ROWBLOCK (the layout kernels specialise
+//    the naive order); long-row TREE: vector / warp kernels.
 int32_t dacsr_select_variant(const dacsr_stats_t* st, int32_t order) {
   if (!st) return DACSR_VARIANT_STAGED;
   if (order == DACSR_ORDER_TREE && st->mean_len >= 48.0)
     return st->mean_len >= 256.0 ? DACSR_VARIANT_WARP : DACSR_VARIANT_VECTOR16;
-  // warp streams while a 32-row chunk's window stays small enough for
-  // several resident warps per SM (planner sizes the window per matrix)
-  const double chunk = 32.0 * st->mean_len;
-  if (chunk <= 1536.0) return DACSR_VARIANT_WSTREAM;
-  return DACSR_VARIANT_ROWBLOCK;
+  if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) return DACSR_VARIANT_ROWBLOCK;
+  if (st->rows < 4096) return DACSR_VARIANT_SCALAR;
+  if (st->scatter > 0.5 && st->mean_len >= 2.0) return DACSR_VARIANT_TILED;
+  return DACSR_VARIANT_SLICED_PIPE;
 }
 
 int dacsr_plan_chunks(const dacsr_matrix_t* a, int64_t rs, int64_t re, int32_t chunk_rows,

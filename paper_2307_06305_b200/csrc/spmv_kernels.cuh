@@ -821,57 +821,6 @@ __device__ __forceinline__ double slice_row_dot(const Mat<KIND, RP, CI, VT>& m, 
   return acc;
 }
 
-// First batch of a lane's row with offset prediction (SLICED_PRED): the x
-// gathers are issued at the offsets this lane saw in the warp's previous
-// slice — for stencil-like matrices the same, since a warp's slices are W
-// slices apart — together with the entry loads, so a correct guess removes
-// the entries -> gathers round trip.  Wrong guesses (compared after the
-// offsets arrive) are gathered again; guesses are clamped into x so the
-// speculative loads stay in bounds.  pred[] is updated to this slice's
-// offsets.  Results are identical whatever the guesses.
-template <int B, class OT, int KIND, class RP, class CI, class VT, class LI, class LV>
-__device__ __forceinline__ double slice_row_dot_pred(const Mat<KIND, RP, CI, VT>& m, int64_t r,
-                                                     int width, int n, const VT* xr,
-                                                     const LI& li, const LV& lv, OT* pred,
-                                                     OT omin, OT omax) {
-  OT o[B];
-  VT vv[B], xs[B];
-#pragma unroll
-  for (int u = 0; u < B; ++u) {
-    const bool on = u < n;
-    const OT g = pred[u] < omin ? omin : (pred[u] > omax ? omax : pred[u]);
-    xs[u] = on ? ldg(elem_addr(xr, g)) : VT(0);
-    o[u] = on ? static_cast<OT>(li(u)) : OT(0);
-    vv[u] = on ? lv(u) : VT(0);
-  }
-  double acc = 0.0;
-#pragma unroll
-  for (int u = 0; u < B; ++u) {
-    const bool on = u < n;
-    if (on) m.check(r, 0, static_cast<CI>(o[u]));
-    const VT xv = !on ? VT(0) : (o[u] == pred[u] ? xs[u] : ldg(elem_addr(xr, o[u])));
-    if (on) pred[u] = o[u];
-    acc = __dadd_rn(acc, product(vv[u], xv));
-  }
-  if (width > B)
-    acc = slice_row_dot<B, OT>(m, r, width, n, xr, li, lv, B, acc);
-  return acc;
-}
-
-// Per-warp staging of the sliced layout: kStages slots of one slice each
-// (values, then inner indices), slices up to `wcap` entries per lane.
-template <class CI, class VT>
-struct SliceStage {
-  static constexpr int kStages = 2;
-  __host__ __device__ static constexpr int value_bytes(int wcap) {
-    return 32 * wcap * static_cast<int>(sizeof(VT));
-  }
-  __host__ __device__ static constexpr int slot_bytes(int wcap) {
-    return value_bytes(wcap) + ((32 * wcap * static_cast<int>(sizeof(CI)) + 15) & ~15);
-  }
-  __host__ __device__ static constexpr int warp_bytes(int wcap) { return kStages * slot_bytes(wcap); }
-};
-
 // Medium slices t = first, first + stride, ... (32 listed rows each; lanes
 // whose row is outside [rs, re) skip), straight from HBM.  Call after
 // griddepcontrol.wait.
@@ -906,22 +855,20 @@ __device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, co
 
 // SLICED kernel.  Each warp first takes its share of the medium slices
 // (rows outside [rs, re) skipped lane by lane), then its main slices of
-// [rs, re); long rows go to the first side_ctas CTAs.  The mode (TMA):
+// [rs, re); long rows go to the first side_ctas CTAs.  PIPE selects:
 //  0  SLICED: every slice straight from HBM with coalesced loads; the
 //     entries of the slice two steps ahead are pulled into L2 by a bulk
 //     prefetch (slice metadata is loaded one step earlier still).
-//  1  SLICED_TMA: each warp keeps the entries of its next two slices in
-//     flight in its shared-memory stages (cp.async.bulk + mbarrier, issued
-//     by lane 0), so only the x gathers sit in registers; slices wider
-//     than wcap are read from HBM as in mode 0.
-//  3  SLICED_PRED: mode 0 with offset-predicted first-batch gathers
-//     (slice_row_dot_pred), 80 registers.
-//  4  SLICED_PIPE: mode 0 with the next slice's first-batch offsets loaded
+//  1  SLICED_PIPE: mode 0 with the next slice's first-batch offsets loaded
 //     while this slice's gathers and values are in flight (one memory round
 //     per slice instead of two), 80 registers.
-#ifndef DACSR_SLICED_PRED_MINB
-#define DACSR_SLICED_PRED_MINB 3
-#endif
+// (Round 1 also had TMA-staged, warp-specialised-ring and offset-predicted
+// modes; each was exact and slower on every BASELINE config — DESIGN.md
+// keeps the measurements — and they were removed.)
+// Programmatic dependent launch: slice metadata and operator loads may run
+// before griddepcontrol.wait; the layout builders synchronize the stream
+// before a layout is used, so the grid before a sliced launch never writes
+// the operator arrays.
 // SLICED_PIPE holds the next slice's offsets across the iteration: 80
 // registers, 3 CTAs/SM (measured: 64 registers spill and run 27 % slower)
 #ifndef DACSR_SLICED_PIPE_MINB
@@ -930,15 +877,12 @@ __device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, co
 #ifndef DACSR_SLICED_PIPE_VALUES
 #define DACSR_SLICED_PIPE_VALUES 1
 #endif
-template <int KIND, class RP, class CI, class VT, int TMA>
-__global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
-                                       : TMA == 4 ? DACSR_SLICED_PIPE_MINB
-                                                  : SlicedTune<VT>::minb)
+template <int KIND, class RP, class CI, class VT, int PIPE>
+__global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTune<VT>::minb)
     sliced_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs, int64_t re,
-                  int side_ctas, int wcap, int flags) {
+                  int side_ctas, int flags) {
   constexpr int B = SlicedTune<VT>::batch;
   using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
-  using SS = SliceStage<CI, VT>;
   extern __shared__ __align__(128) unsigned char dsm[];
   // programmatic dependent launch: metadata and operator loads may start
   // while the previous grid drains; x / y only after griddepcontrol.wait
@@ -949,7 +893,6 @@ __global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
               reinterpret_cast<double*>(dsm));
     return;
   }
-  __shared__ __align__(8) uint64_t bars[8][SS::kStages];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t W = static_cast<int64_t>(gridDim.x - side_ctas) * (blockDim.x >> 5);
   const int64_t gw = static_cast<int64_t>(blockIdx.x - side_ctas) * (blockDim.x >> 5) + wib;
@@ -967,13 +910,6 @@ __global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
   // main slices of [rs, re)
   int64_t c = s0 + gw;
   if (c >= s1) return;
-  unsigned char* wbase = dsm + (TMA == 1 ? wib * SS::warp_bytes(wcap) : 0);
-  uint64_t* bar = bars[wib];
-  if (TMA == 1 && lane == 0) {
-    for (int k = 0; k < SS::kStages; ++k) mbar_init(&bar[k], 1);
-    mbar_fence_init();
-  }
-  __syncwarp();
   // slice metadata: raw loads now, arithmetic one iteration later (so the
   // loads are never waited on where they are issued).  l: the lane's row
   // length byte; 256 = not a row of this launch.
@@ -1002,32 +938,22 @@ __global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
     q.n = w.l > sl.max_len ? -1 : w.l;  // 256 (none) or a medium / long row
     return q;
   };
-  auto is_staged = [&](const Meta& q) { return TMA == 1 && q.width > 0 && q.width <= wcap; };
-  // lane 0: the slice's two arrays into stage `slot` (TMA), or into L2
-  auto stage = [&](const Meta& q, int slot) {
+  // lane 0: the slice's two arrays into L2 (bulk prefetch)
+  auto stage = [&](const Meta& q) {
     if (lane != 0 || q.width <= 0) return;
-    const uint32_t vb = static_cast<uint32_t>(32 * q.width * sizeof(VT));
-    const uint32_t ib = static_cast<uint32_t>((32 * q.width * sizeof(CI) + 15) & ~size_t(15));
-    if (is_staged(q)) {
-      unsigned char* dst = wbase + slot * SS::slot_bytes(wcap);
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&bar[slot], vb + ib);
-      bulk_copy_g2s(dst, sl.v + q.p0, vb, &bar[slot]);
-      bulk_copy_g2s(dst + SS::value_bytes(wcap), sl.ci + q.p0, ib, &bar[slot]);
-    } else if (DACSR_SLICED_PREFETCH && !(flags & DACSR_PLAN_NO_L2_PREFETCH)) {
-      prefetch_l2_bulk(sl.v + q.p0, vb);
+    if (DACSR_SLICED_PREFETCH && !(flags & DACSR_PLAN_NO_L2_PREFETCH)) {
+      prefetch_l2_bulk(sl.v + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(VT)));
       prefetch_l2_bulk(sl.ci + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(CI)) & ~15u);
     }
   };
-  if constexpr (TMA == 4) {
+  if constexpr (PIPE) {
     // offsets one slice ahead: the first batch's offsets of the next slice
     // are loaded while this slice's gathers and values are in flight, so
     // each slice costs one memory round (gathers + values) instead of two
-    // (offsets, then gathers).  Only the offsets (not the values) are held
-    // across the iteration, which keeps the batch within 64 registers.
+    // (offsets, then gathers).
     Meta cur = derive(load_raw(c));
     Meta nxt = derive(load_raw(c + W));
-    stage(nxt, 1);
+    stage(nxt);
     OT oc[B];
     // f32 values are cheap to hold too: the next slice's first-batch values
     // travel with its offsets (measured: f32 -5 % time; f64 would spill,
@@ -1077,7 +1003,7 @@ __global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
       }
       if (cur.n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
       const Meta nxt2 = derive(raw2);
-      stage(nxt2, 0);
+      stage(nxt2);
       cur = nxt;
       nxt = nxt2;
     }
@@ -1085,15 +1011,9 @@ __global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
   }
   Meta cur = derive(load_raw(c));
   Meta nxt = derive(load_raw(c + W));
-  if (TMA == 1) stage(cur, 0);
-  stage(nxt, 1);
+  stage(nxt);
   if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
-  uint32_t phase = 0;
-  OT pred[B];
-#pragma unroll
-  for (int u = 0; u < B; ++u) pred[u] = OT(0);
-  for (int k = 0; c < s1; c += W, ++k) {
-    const int slot = k & 1;
+  for (; c < s1; c += W) {
     const Raw raw2 = load_raw(c + 2 * W);
     const int64_t r = sl.row0 + 32 * c + lane;
     const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
@@ -1102,181 +1022,29 @@ __global__ void __launch_bounds__(256, TMA == 3   ? DACSR_SLICED_PRED_MINB
     asm("" : "+l"(xr));
     DACSR_CHECK(cur.n <= cur.width && cur.width <= 254);
     DACSR_CHECK(cur.n <= 0 || cur.p0 + lane + 32 * (cur.n - 1) < sl.total);
+    const CI* pi = sl.ci + cur.p0 + lane;
+    const VT* pv = sl.v + cur.p0 + lane;
     double acc;
-    if (is_staged(cur)) {
-      mbar_wait(&bar[slot], (phase >> slot) & 1u);
-      phase ^= 1u << slot;
-      const unsigned char* base = wbase + slot * SS::slot_bytes(wcap);
-      const VT* pv = reinterpret_cast<const VT*>(base) + lane;
-      const CI* pi = reinterpret_cast<const CI*>(base + SS::value_bytes(wcap)) + lane;
+    if (DACSR_SLICED_LDCS)
       acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
-                                 [&](int j) { return pi[32 * j]; },
-                                 [&](int j) { return pv[32 * j]; });
-    } else if (TMA == 3) {
-      const CI* pi = sl.ci + cur.p0 + lane;
-      const VT* pv = sl.v + cur.p0 + lane;
-      // valid guesses keep the column inside x (x_offset is 0 in this mode)
-      const OT omin = KIND == DACSR_KIND_DA ? static_cast<OT>(-r) : OT(0);
-      const OT omax = static_cast<OT>((KIND == DACSR_KIND_DA ? m.ncols - 1 - r : m.ncols - 1));
-      acc = slice_row_dot_pred<B, OT>(m, r, cur.width, cur.n, xr,
-                                      [&](int j) { return ldcs(pi + 32 * j); },
-                                      [&](int j) { return ldcs(pv + 32 * j); }, pred, omin,
-                                      omax);
-    } else {
-      const CI* pi = sl.ci + cur.p0 + lane;
-      const VT* pv = sl.v + cur.p0 + lane;
-      if (DACSR_SLICED_LDCS)
-        acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
-                                   [&](int j) { return ldcs(pi + 32 * j); },
-                                   [&](int j) { return ldcs(pv + 32 * j); });
-      else
-        acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
-                                   [&](int j) { return ldg(pi + 32 * j); },
-                                   [&](int j) { return ldg(pv + 32 * j); });
-    }
+                                 [&](int j) { return ldcs(pi + 32 * j); },
+                                 [&](int j) { return ldcs(pv + 32 * j); });
+    else
+      acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
+                                 [&](int j) { return ldg(pi + 32 * j); },
+                                 [&](int j) { return ldg(pv + 32 * j); });
     if (cur.n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
-    __syncwarp();  // every lane is done with this slot before it is refilled
     const Meta nxt2 = derive(raw2);
-    stage(nxt2, slot);
+    stage(nxt2);
     cur = nxt;
     nxt = nxt2;
   }
 }
 
-// ------------------------------------------- SLICED_RING (warp-specialised)
-// One producer warp per CTA streams chunks of K consecutive main slices —
-// their values, inner indices, slice_ptr entries and row-length bytes, four
-// bulk copies per chunk — into an nstages-deep shared-memory ring (full /
-// empty mbarriers); the consumer warps take the chunk's slices round robin
-// and fold them from shared memory (lane l reads slot 32j + l: no bank
-// conflicts), gathering x from L2.  Large copies keep the DRAM stream dense
-// and no entry bytes occupy registers in flight.  The first side_ctas CTAs
-// take the medium slices and the long rows.
-// 16 consumer warps, 3 stages of <= 36 KiB, 2 CTAs/SM (measured best of
-// 8/16 consumers x 2/3/4 stages on C2 / C2-f32 / C2-bf16 / C4)
-#ifndef DACSR_RING_CONSUMERS
-#define DACSR_RING_CONSUMERS 16
-#endif
-constexpr int kRingMaxStages = 8;
-constexpr int kRingConsumers = DACSR_RING_CONSUMERS;
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-template <class CI, class VT>
-struct RingStage {
-  // [values: vcap][inner: vcap, 16B-rounded][slice_ptr: K + 2][row_len: 32 K]
-  __host__ __device__ static constexpr int inner_off(int vcap) {
-    return (vcap * static_cast<int>(sizeof(VT)) + 15) & ~15;
-  }
-  __host__ __device__ static constexpr int ptr_off(int vcap) {
-    return inner_off(vcap) + ((vcap * static_cast<int>(sizeof(CI)) + 15) & ~15);
-  }
-  __host__ __device__ static constexpr int len_off(int vcap, int K) {
-    return ptr_off(vcap) + ((K + 2) * 8 + 15) / 16 * 16;
-  }
-  __host__ __device__ static constexpr int bytes(int vcap, int K) {
-    return len_off(vcap, K) + 32 * K;
-  }
-};
-
-template <int KIND, class RP, class CI, class VT>
-__global__ void __launch_bounds__(32 * (kRingConsumers + 1), 2)
-    sliced_ring_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs,
-                       int64_t re, int side_ctas, int K, int vcap, int nstages) {
-  constexpr int B = SlicedTune<VT>::batch;
-  using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
-  using RS = RingStage<CI, VT>;
-  extern __shared__ __align__(128) unsigned char dsm[];
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (static_cast<int>(blockIdx.x) < side_ctas) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int nw = blockDim.x >> 5;
-    medium_slices<B, OT>(m, s, sl, rs, re, static_cast<int64_t>(blockIdx.x) * nw + warp,
-                         static_cast<int64_t>(side_ctas) * nw, lane);
-    long_rows(m, s, rs, re, sl.lrows, sl.n_long, blockIdx.x, side_ctas,
-              reinterpret_cast<double*>(dsm));
-    return;
-  }
-  __shared__ __align__(8) uint64_t full[kRingMaxStages], empty[kRingMaxStages];
-  const int64_t s0 = (rs - sl.row0) >> 5, s1 = (re - sl.row0 + 31) >> 5;
-  const int64_t nchunks = (s1 - s0 + K - 1) / K;
-  const int cta = blockIdx.x - side_ctas, ncta = gridDim.x - side_ctas;
-  const int sbytes = RS::bytes(vcap, K);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < nstages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kRingConsumers);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (warp == kRingConsumers) {  // producer
-    if (lane == 0) {
-      int i = 0;
-      for (int64_t k = cta; k < nchunks; k += ncta, ++i) {
-        const int st = i % nstages;
-        if (i >= nstages) mbar_wait(&empty[st], static_cast<uint32_t>((i / nstages - 1) & 1));
-        const int64_t c0 = s0 + k * K, c1 = min64(c0 + K, s1);
-        const int64_t p0 = ldg(sl.ptr + c0), p1 = ldg(sl.ptr + c1);
-        const uint32_t slots = static_cast<uint32_t>(p1 - p0);
-        const int64_t ps = c0 & ~int64_t(1);                 // 16-byte aligned start
-        const uint32_t pn = static_cast<uint32_t>(((c1 + 1 - ps) + 1) & ~int64_t(1));
-        const uint32_t vb = slots * static_cast<uint32_t>(sizeof(VT));
-        const uint32_t ib = (slots * static_cast<uint32_t>(sizeof(CI)) + 15) & ~15u;
-        const uint32_t lb = static_cast<uint32_t>(32 * (c1 - c0));
-        unsigned char* dst = dsm + st * sbytes;
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&full[st], (vb > 0 ? vb + ib : 0) + pn * 8 + lb);
-        if (vb > 0) {
-          bulk_copy_g2s(dst, sl.v + p0, vb, &full[st]);
-          bulk_copy_g2s(dst + RS::inner_off(vcap), sl.ci + p0, ib, &full[st]);
-        }
-        bulk_copy_g2s(dst + RS::ptr_off(vcap), sl.ptr + ps, pn * 8, &full[st]);
-        bulk_copy_g2s(dst + RS::len_off(vcap, K), sl.len + 32 * c0, lb, &full[st]);
-      }
-    }
-    return;
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y from here on
-  const VT* __restrict__ xb = m.x + m.xoff;
-  int i = 0;
-  for (int64_t k = cta; k < nchunks; k += ncta, ++i) {
-    const int st = i % nstages;
-    mbar_wait(&full[st], static_cast<uint32_t>((i / nstages) & 1));
-    const unsigned char* base = dsm + st * sbytes;
-    const int64_t c0 = s0 + k * K, c1 = min64(c0 + K, s1);
-    const int64_t* sp = reinterpret_cast<const int64_t*>(base + RS::ptr_off(vcap)) + (c0 & 1);
-    const uint8_t* ln = base + RS::len_off(vcap, K);
-    const int64_t pc = sp[0];
-    for (int q = warp; q < c1 - c0; q += kRingConsumers) {
-      const int64_t c = c0 + q;
-      const int64_t p0 = sp[q];
-      const int width = static_cast<int>((sp[q + 1] - p0) >> 5);
-      const int64_t r = sl.row0 + 32 * c + lane;
-      int n = -1;
-      if (r >= rs && r < re) {
-        const int l = ln[32 * q + lane];
-        n = l > sl.max_len ? -1 : l;
-      }
-      const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
-      asm("" : "+l"(xr));
-      DACSR_CHECK(n <= width && width <= 254 && p0 - pc + 32 * width <= vcap);
-      const VT* pv = reinterpret_cast<const VT*>(base) + (p0 - pc) + lane;
-      const CI* pi = reinterpret_cast<const CI*>(base + RS::inner_off(vcap)) + (p0 - pc) + lane;
-      const double acc = slice_row_dot<B, OT>(m, r, width, n, xr,
-                                              [&](int j) { return pi[32 * j]; },
-                                              [&](int j) { return pv[32 * j]; });
-      if (n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
-}
-
-// planner: list the 32-row chunks that do not fit a VCAP window
 template <class RP>
 __global__ void classify_chunks_kernel(const RP* __restrict__ rp, int64_t rs, int64_t re,
                                        int rows, int vcap, int align, int64_t last_aligned,
@@ -1317,38 +1085,48 @@ int launch_values_bf16(const dacsr_matrix_t* a, const Req& q);
 // ============================================================ host side
 namespace {
 
-int sm_count() {
-  static int cached = -1;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
+int current_device() {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  if (cached < 0) {
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  return dev;
+}
+
+// SM count of the current device (cached per device)
+int sm_count() {
+  static int cached[64];
+  static bool have[64];
+  static std::mutex mu;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!have[dev]) {
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
       v = 148;
-    cached = v;
+    cached[dev] = v;
+    have[dev] = true;
   }
-  return cached;
+  return cached[dev];
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-// the sliced arrays start 16-byte aligned (slices then start at multiples
-// of 32 entries, so every slice is a legal bulk-copy source)
-bool can_bulk_sl(const dacsr_slices_t* sd) { return aligned16(sd->values) && aligned16(sd->inner); }
 
-// Per-kernel launch configuration, computed once per (kernel, smem bytes):
-// the max-dynamic-smem attribute and the occupancy query cost microseconds
-// of host time, which would otherwise sit between back-to-back launches.
-// The attribute is raised once per kernel to the device's opt-in maximum
-// (it is a cap, not a reservation), so cached entries stay launchable.
+// Per-kernel launch configuration, computed once per (device, kernel, smem
+// bytes): the max-dynamic-smem attribute and the occupancy query cost
+// microseconds of host time, which would otherwise sit between back-to-back
+// launches.  Function attributes are per device, so the attribute is raised
+// once per (device, kernel) to that device's opt-in maximum (a cap, not a
+// reservation), which keeps cached entries launchable.
 struct LaunchCache {
   std::mutex mu;
-  const void* fn[96] = {};
-  size_t smem[96] = {};
-  int per_sm[96] = {};
+  static constexpr int kMax = 256;
+  const void* fn[kMax] = {};
+  int dev[kMax] = {};
+  size_t smem[kMax] = {};
+  int per_sm[kMax] = {};
   int n = 0;
-  const void* raised[96] = {};
+  const void* raised[kMax] = {};
+  int raised_dev[kMax] = {};
   int n_raised = 0;
 };
 
@@ -1356,29 +1134,34 @@ template <class K>
 int cached_per_sm(K kern, int threads, size_t smem) {
   static LaunchCache cache;
   const void* key = reinterpret_cast<const void*>(kern);
+  const int dev = current_device();
   std::lock_guard<std::mutex> lock(cache.mu);
   for (int i = 0; i < cache.n; ++i)
-    if (cache.fn[i] == key && cache.smem[i] == smem) return cache.per_sm[i];
+    if (cache.fn[i] == key && cache.dev[i] == dev && cache.smem[i] == smem) return cache.per_sm[i];
   bool raised = false;
-  for (int i = 0; i < cache.n_raised; ++i) raised |= cache.raised[i] == key;
+  for (int i = 0; i < cache.n_raised; ++i)
+    raised |= cache.raised[i] == key && cache.raised_dev[i] == dev;
   if (!raised) {
-    int dev = 0, optin = 227 * 1024;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    int optin = 227 * 1024;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return -1;
     const int dyn_max = optin - static_cast<int>(fa.sharedSizeBytes);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) !=
         cudaSuccess)
       return -1;
-    if (cache.n_raised < 96) cache.raised[cache.n_raised++] = key;
+    if (cache.n_raised < LaunchCache::kMax) {
+      cache.raised[cache.n_raised] = key;
+      cache.raised_dev[cache.n_raised++] = dev;
+    }
   }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess)
     return -1;
   per_sm = std::max(1, per_sm);
-  if (cache.n < 96) {
+  if (cache.n < LaunchCache::kMax) {
     cache.fn[cache.n] = key;
+    cache.dev[cache.n] = dev;
     cache.smem[cache.n] = smem;
     cache.per_sm[cache.n] = per_sm;
     ++cache.n;
@@ -1393,61 +1176,6 @@ int rowblock_stages(int cap) {
   const size_t budget = 100 * 1024;
   int st = static_cast<int>(budget / stage);
   return std::max(2, std::min(kMaxStages, st));
-}
-
-#ifndef DACSR_RING_STAGE_BYTES
-#define DACSR_RING_STAGE_BYTES (36 * 1024)
-#endif
-#ifndef DACSR_RING_STAGES
-#define DACSR_RING_STAGES 3
-#endif
-template <int KIND, class RP, class CI, class VT>
-int launch_ring(const Mat<KIND, RP, CI, VT>& m, const Scal& s, const SliceArgs<CI, VT>& sa,
-                const dacsr_slices_t* sd, const dacsr_plan_t* p, const Req& q, int sms) {
-  using RS = RingStage<CI, VT>;
-  // K slices per chunk: a multiple of the 8 consumer warps when a stage of
-  // that size fits the budget, else as many as fit (at least one)
-  const int per_slice = 32 * std::max(1, static_cast<int>(sd->max_len)) *
-                        static_cast<int>(sizeof(VT) + sizeof(CI));
-  int K = DACSR_RING_STAGE_BYTES / (per_slice + 40);
-  if (K >= kRingConsumers) K -= K % kRingConsumers;
-  K = std::max(1, std::min(K, 64));
-  const int vcap = 32 * K * std::max(1, static_cast<int>(sd->max_len));
-  int nstages = DACSR_RING_STAGES;
-  while (nstages > 2 && static_cast<size_t>(nstages) * RS::bytes(vcap, K) > 200 * 1024) --nstages;
-  const size_t ring_bytes = static_cast<size_t>(nstages) * RS::bytes(vcap, K);
-  const int threads = 32 * (kRingConsumers + 1);
-  const size_t side_bytes = sd->n_long > 0 ? static_cast<size_t>(threads / 32) * 128 * 8 : 0;
-  const size_t smem = std::max(ring_bytes, side_bytes);
-  auto kern = sliced_ring_kernel<KIND, RP, CI, VT>;
-  int per_sm = cached_per_sm(kern, threads, smem);
-  if (per_sm < 0) return check_launch("sliced_ring launch config");
-  if (p->ctas_per_sm > 0) per_sm = std::min(per_sm, static_cast<int>(p->ctas_per_sm));
-  const int64_t slots = static_cast<int64_t>(sms) * per_sm;
-  const int64_t nsl = ((q.re - sd->row_start + 31) >> 5) - ((q.rs - sd->row_start) >> 5);
-  const int64_t nchunks = (nsl + K - 1) / K;
-  const int64_t side_work = sd->m_nslices + sd->n_long;
-  const int side = side_work > 0 ? static_cast<int>(std::min<int64_t>(
-                                       (side_work + 2 * kRingConsumers - 1) / (2 * kRingConsumers),
-                                       std::max<int64_t>(1, slots / 8)))
-                                 : 0;
-  const int64_t grid = std::min<int64_t>(nchunks, std::max<int64_t>(slots - side, slots / 2));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(grid, 1) + side));
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = q.stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, sa, q.rs, q.re, side, K, vcap, nstages);
-  if (e != cudaSuccess) {
-    set_last_error("sliced_ring_kernel launch", e);
-    return DACSR_ERR_CUDA;
-  }
-  return check_launch("sliced_ring_kernel");
 }
 
 template <int KIND, class RP, class CI, class VT>
@@ -1582,9 +1310,6 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       return check_launch("wstream_kernel");
     }
     case DACSR_VARIANT_SLICED:
-    case DACSR_VARIANT_SLICED_TMA:
-    case DACSR_VARIANT_SLICED_RING:
-    case DACSR_VARIANT_SLICED_PRED:
     case DACSR_VARIANT_SLICED_PIPE: {
       const dacsr_plan_t* p = q.plan;
       if (!p || !p->slices) return DACSR_ERR_PLAN;
@@ -1610,31 +1335,10 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
                            sd->max_len, sd->medium_rows, sd->m_slice_ptr,
                            static_cast<const CI*>(sd->m_inner), static_cast<const VT*>(sd->m_values),
                            sd->n_medium, sd->m_nslices, sd->m_total, sd->long_rows, sd->n_long};
-      if (q.variant == DACSR_VARIANT_SLICED_RING)
-        return launch_ring<KIND, RP, CI, VT>(m, s, sa, sd, p, q, sms);
       constexpr int warps = 8, threads = 32 * warps;
-      using SS = SliceStage<CI, VT>;
-      const bool tma = q.variant == DACSR_VARIANT_SLICED_TMA && can_bulk_sl(sd);
-      // stage width: the layout's longest kept row, within ~56 KiB of
-      // stages per CTA (4 CTAs per SM)
-      int wcap = 0;
-      if (tma) {
-        const int per_entry = 32 * SS::kStages * warps * static_cast<int>(sizeof(VT) + sizeof(CI));
-        wcap = std::max(1, std::min<int>(sd->max_len, (56 * 1024) / per_entry));
-      }
-      const size_t stage_bytes = tma ? static_cast<size_t>(warps) * SS::warp_bytes(wcap) : 0;
-      const size_t side_bytes = sd->n_long > 0 ? static_cast<size_t>(warps) * 128 * 8 : 0;
-      const size_t smem = std::max(stage_bytes, side_bytes);
-      // prediction needs the true x extent (no rank-local x_offset)
-      const bool pred = q.variant == DACSR_VARIANT_SLICED_PRED && q.xoff == 0 && a->ncols > 0;
-#ifndef DACSR_SLICED_DEFAULT_MODE
-#define DACSR_SLICED_DEFAULT_MODE 0
-#endif
-      auto kern = tma    ? sliced_kernel<KIND, RP, CI, VT, 1>
-                  : pred ? sliced_kernel<KIND, RP, CI, VT, 3>
-                  : q.variant == DACSR_VARIANT_SLICED_PIPE
-                      ? sliced_kernel<KIND, RP, CI, VT, 4>
-                      : sliced_kernel<KIND, RP, CI, VT, DACSR_SLICED_DEFAULT_MODE>;
+      const size_t smem = sd->n_long > 0 ? static_cast<size_t>(warps) * 128 * 8 : 0;
+      auto kern = q.variant == DACSR_VARIANT_SLICED_PIPE ? sliced_kernel<KIND, RP, CI, VT, 1>
+                                                         : sliced_kernel<KIND, RP, CI, VT, 0>;
       int per_sm = cached_per_sm(kern, threads, smem);
       if (per_sm < 0) return check_launch("sliced launch config");
       if (p->ctas_per_sm > 0) per_sm = std::min(per_sm, static_cast<int>(p->ctas_per_sm));
@@ -1658,7 +1362,7 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, sa, q.rs, q.re, side, wcap,
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m, s, sa, q.rs, q.re, side,
                                          static_cast<int>(p->flags));
       if (e != cudaSuccess) {
         set_last_error("sliced_kernel launch", e);

@@ -110,42 +110,6 @@ __device__ __forceinline__ const T* elem_addr_u32(const T* base, uint32_t o) {
   return p;
 }
 
-// predicated evict-first load (asm volatile: issued in program order, so a
-// batch's loads all leave before the batch folds); 0 when !pred
-template <class T>
-struct LdCs;
-#define DACSR_LDCS_PRED(T, R, C, SUF)                                                  \
-  template <>                                                                          \
-  struct LdCs<T> {                                                                     \
-    using reg = R;                                                                     \
-    __device__ __forceinline__ static R load(const T* p, bool pred) {                  \
-      R v = 0;                                                                         \
-      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cs." SUF \
-                   " %0, [%1];\n\t}"                                                  \
-                   : "+" C(v)                                                          \
-                   : "l"(p), "r"(static_cast<unsigned>(pred)));                        \
-      return v;                                                                        \
-    }                                                                                  \
-  };
-DACSR_LDCS_PRED(int8_t, int, "r", "s8")
-DACSR_LDCS_PRED(int16_t, int, "r", "s16")
-DACSR_LDCS_PRED(int32_t, int, "r", "s32")
-DACSR_LDCS_PRED(int64_t, long long, "l", "s64")
-DACSR_LDCS_PRED(double, double, "d", "f64")
-DACSR_LDCS_PRED(float, float, "f", "f32")
-DACSR_LDCS_PRED(unsigned short, unsigned short, "h", "b16")
-#undef DACSR_LDCS_PRED
-template <class T, class OUT>
-__device__ __forceinline__ OUT ld_cs_pred(const T* p, bool pred) {
-  if constexpr (std::is_same<T, __half>::value)
-    return __ushort_as_half(LdCs<unsigned short>::load(reinterpret_cast<const unsigned short*>(p), pred));
-  else if constexpr (std::is_same<T, __nv_bfloat16>::value)
-    return __ushort_as_bfloat16(
-        LdCs<unsigned short>::load(reinterpret_cast<const unsigned short*>(p), pred));
-  else
-    return static_cast<OUT>(LdCs<T>::load(p, pred));
-}
-
 // Predicated evict-first load of two consecutive elements (one vector load;
 // p aligned to 2 * sizeof(T)); asm volatile, so a batch's loads are issued
 // in program order before the batch folds.  Outputs are undefined when

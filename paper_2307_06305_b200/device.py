@@ -28,7 +28,10 @@ from . import _native
 from .core import CsrMatrix, DacsrMatrix
 
 # kernels that run on the sliced layout (DeviceMatrix.build_slices)
-SLICED_KERNELS = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe")
+SLICED_KERNELS = ("sliced", "sliced_pipe")
+# kernels on a derived layout of the whole row range (any launch row range
+# inside it): the sliced layout and the band-tiled layout
+LAYOUT_KERNELS = SLICED_KERNELS + ("tiled",)
 
 _KIND_NAME = {_native.KIND_CSR: "csr", _native.KIND_DA: "da"}
 
@@ -47,6 +50,10 @@ def _upload(arr, dtype, device):
     if not a.flags.writeable:
         a = a.copy()
     return torch.from_numpy(a).to(device)
+
+
+def _sync(stream=None):
+    (stream if stream is not None else torch.cuda.current_stream()).synchronize()
 
 
 def _stream_ptr(stream=None):
@@ -254,7 +261,7 @@ class DeviceMatrix:
         ``max_len`` entries sit in main slices, rows up to ``medium_len``
         (default max(max_len, 32)) in medium slices of 32 listed rows, longer
         rows are reduced warp by warp.  Returns the plan that carries it
-        (variants "sliced" / "sliced_tma")."""
+        (variants "sliced" / "sliced_pipe")."""
         L = _native.lib()
         if self.plan is None:
             self.build_plan(stream=stream)
@@ -269,8 +276,7 @@ class DeviceMatrix:
         dev = self.device
         sp = _stream_ptr(stream)
         vp = lambda t: ctypes.c_void_p(t.data_ptr())
-        # padded for SLICED_RING's bulk copies: 32 bytes per slice, slice_ptr + 1
-        row_len = torch.zeros(max(32 * ns, 1), dtype=torch.uint8, device=dev)
+        row_len = torch.zeros(max(re - rs, 1), dtype=torch.uint8, device=dev)
         counts = torch.zeros(3, max(ns, 1), dtype=torch.int32, device=dev)
         ptrs = torch.zeros(3, ns + 2, dtype=torch.int64, device=dev)
         with torch.cuda.device(dev):
@@ -305,6 +311,10 @@ class DeviceMatrix:
                 sl.m_total, sl.m_inner, sl.m_values = m_total, m_inner.data_ptr(), m_values.data_ptr()
                 _native.check(L.dacsr_slices_medium_fill(ctypes.byref(self.desc), ctypes.byref(sl),
                                                          sp), "dacsr_slices_medium_fill")
+            # the sliced kernels use programmatic dependent launch and read
+            # the operator before griddepcontrol.wait: the layout must be
+            # complete before any launch that follows
+            _sync(stream)
         plan = _native.Plan()
         ctypes.memmove(ctypes.byref(plan), ctypes.byref(self.plan), ctypes.sizeof(plan))
         plan.slices = ctypes.addressof(sl)
@@ -370,6 +380,7 @@ class DeviceMatrix:
             tl.ovf_rows = ovf_rows.data_ptr()
             _native.check(L.dacsr_tiles_fill(ctypes.byref(self.desc), ctypes.byref(tl),
                                               vp(ptrs[2]), sp), "dacsr_tiles_fill")
+            _sync(stream)
         plan = _native.Plan()
         ctypes.memmove(ctypes.byref(plan), ctypes.byref(self.plan), ctypes.sizeof(plan))
         plan.slices = self._sliced[0].slices if self._sliced is not None else None
@@ -411,15 +422,16 @@ class DeviceMatrix:
                 "bytes": sum(t.numel() * t.element_size() for t in tensors.values()
                              if t is not None)}
 
-    def autotune(self, candidates=("sliced", "sliced_pipe", "sliced_pred", "sliced_ring",
-                                   "sliced_tma", "wstream", "scalar", "rowblock", "staged"),
-                 cold=False,
-                 x=None, reps=5, tune_layout=True):
+    def autotune(self, candidates=("tiled", "sliced_pipe", "sliced", "wstream", "scalar",
+                                   "rowblock"),
+                 cold=False, x=None, reps=5, tune_layout=True):
         """Time the exact naive-order kernels on this matrix and remember the
         fastest for variant "naive"/"auto" (all give bit-identical results,
-        so this only changes speed).  With ``tune_layout`` the sliced
-        layout's width (max_len) is chosen too; otherwise the current layout
-        is kept.  Returns {kernel: seconds}."""
+        so this only changes speed; without autotune the row-statistics
+        selection of dacsr_select_variant applies).  With ``tune_layout``
+        the sliced layout's width (max_len) and its L2-prefetch flag are
+        chosen too; otherwise the current layout is kept.  Derived layouts
+        of kernels that lose are released.  Returns {kernel: seconds}."""
         from .harness import time_kernel
         if x is None:
             x = torch.ones(self.ncols, dtype=self.values.dtype, device=self.device)
@@ -431,54 +443,40 @@ class DeviceMatrix:
             return time_kernel(fn, epochs=3, warmup_iters=2, min_epoch_iters=reps,
                                min_epoch_time=0.0, cold=cold, graph=0 if cold else reps)
 
-        if tune_layout and "sliced" in candidates and self.plan is not None and self.nnz:
+        sliced = [k for k in candidates if k in SLICED_KERNELS]
+        flag = True
+        if tune_layout and sliced and self.plan is not None and self.nnz:
             # the main/medium split changes the slice widths a warp walks:
             # time the cost model's choice against 8 and 16 (one batch or
-            # two per slice) and keep the fastest layout
-            # (timed with SLICED_PIPE, the usual winner, with and without
-            # the L2 prefetch: C5 prefers 16 without it, C2 7 with it)
+            # two per slice), each with and without the L2 prefetch, and keep
+            # the fastest (layout, flag)
             model = self.slice_max_len()
             longest = int(self.stats.max_len) if self.stats is not None else 254
-            probe = "sliced_pipe" if "sliced_pipe" in candidates else "sliced"
+            probe = "sliced_pipe" if "sliced_pipe" in sliced else sliced[0]
             tried = {}
-            for t in sorted({model, 8, 16}):
-                t = min(t, max(1, longest))
-                if (t, True) in tried:
-                    continue
+            for t in sorted({min(v, max(1, longest)) for v in (model, 8, 16)}):
                 self.build_slices(t)
-                tried[(t, True)] = timed(probe)
-                self.set_sliced_l2_prefetch(False)
-                tried[(t, False)] = timed(probe)
-            best_t, _ = min(tried, key=tried.get)
-            if self._sliced is None or self._sliced[1].max_len != best_t:
+                for on in (True, False):
+                    self.set_sliced_l2_prefetch(on)
+                    tried[(t, on)] = timed(probe)
+            (best_t, flag), _ = min(tried.items(), key=lambda kv: kv[1])
+            if self._sliced[1].max_len != best_t:
                 self.build_slices(best_t)
             self.slice_max_len_tuned = {f"{k[0]}{'' if k[1] else ':no_l2_prefetch'}": v
                                         for k, v in tried.items()}
+        if self._sliced is not None:
+            self.set_sliced_l2_prefetch(flag)
         for k in candidates:
-            if k in times:
-                continue
-            if (k in ("wstream", "rowblock") or k in SLICED_KERNELS) and self.plan is None:
+            if k in ("wstream", "rowblock", "tiled") + SLICED_KERNELS and self.plan is None:
                 continue
             times[k] = timed(k)
-        if self._sliced is not None:
-            # the L2 bulk prefetch of the slice two steps ahead helps some
-            # matrices and costs others a few percent: time both
-            self.set_sliced_l2_prefetch(False)
-            for k in ("sliced", "sliced_pipe"):
-                if k in times:
-                    times[k + ":no_l2_prefetch"] = timed(k)
-            self.set_sliced_l2_prefetch(True)
         best = min(times, key=times.get)
-        if best.endswith(":no_l2_prefetch"):
-            best = best.split(":")[0]
-            self.set_sliced_l2_prefetch(False)
         self.tuned_kernel = best
-        if self.tuned_kernel not in SLICED_KERNELS and self._sliced is not None:
-            # the sliced copy of the entries was only built to be timed
-            self._sliced = None
-            self._launch_cache.clear()
-            if getattr(self, "_streamed", None) is not None:
-                self._streamed._plans.clear()
+        if best not in SLICED_KERNELS and self._sliced is not None:
+            self._sliced = None  # the sliced copy of the entries was only built to be timed
+        if best != "tiled" and self._tiled is not None:
+            self._tiled = None
+        self._invalidate_launches()
         return times
 
     def set_sliced_l2_prefetch(self, on):
@@ -491,9 +489,7 @@ class DeviceMatrix:
             plan.flags &= ~_native.PLAN_NO_L2_PREFETCH
         else:
             plan.flags |= _native.PLAN_NO_L2_PREFETCH
-        self._launch_cache.clear()
-        if getattr(self, "_streamed", None) is not None:
-            self._streamed._plans.clear()
+        self._invalidate_launches()
 
     def set_ctas_per_sm(self, n):
         """Cap WSTREAM's resident CTAs per SM (0 = occupancy maximum)."""

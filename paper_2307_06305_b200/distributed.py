@@ -151,7 +151,7 @@ class CudaLocalOp:
 
     def __init__(self, kind, rowptr, colids, values, ncols_global, plan, chunk, b,
                  variant="naive"):
-        from .device import DeviceMatrix
+        from .device import LAYOUT_KERNELS, DeviceMatrix
         from .spmv import kernel_for, resolve_variant
         n_local = rowptr.numel() - 1
         self.n_local = n_local
@@ -163,10 +163,10 @@ class CudaLocalOp:
         name, order = resolve_variant(variant)
         self.order = order
         self.mats = []
-        if name in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe") and n_local:
-            # one sliced layout of all local rows serves the three row ranges
+        if name in LAYOUT_KERNELS and n_local:
+            # one derived layout of all local rows serves the three row ranges
             full = DeviceMatrix(kind, n_local, ncols_global, rowptr, colids, values)
-            full.build_slices()
+            full.build_tiles() if name == "tiled" else full.build_slices()
             self.mats = [full if r1 > r0 else None for r0, r1 in self.ranges]
             self.kernels = [name if r1 > r0 else None for r0, r1 in self.ranges]
         else:

@@ -17,6 +17,7 @@ with the same exact order (each piece is a row range with its own plan).
 import numpy as np
 import torch
 
+from .device import LAYOUT_KERNELS
 from .spmv import kernel_for
 
 
@@ -62,8 +63,8 @@ class StreamedHost:
         if rec is None:
             k = kernel_for(self.dm, kname, order)
             plans = (_native.Plan * len(self.views))()
-            if k in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"):
-                # the pieces share the whole matrix's sliced layout (the
+            if k in LAYOUT_KERNELS:
+                # the pieces share the whole matrix's derived layout (the
                 # kernel takes any row range inside it); no row-block table
                 pl = self.dm.plan_for(k)
                 for i, v in enumerate(self.views):

@@ -48,9 +48,8 @@ _EXACT = {
     "multi_accumulator_3": ("exact", _native.ORDER_MACC3),
     "strip_mined_4": ("exact", _native.ORDER_STRIP4),
 }
-_EXACT_KERNELS = ("rowblock", "staged", "scalar", "wstream", "sliced", "sliced_tma",
-                  "sliced_ring", "sliced_pred", "sliced_pipe", "tiled")
-_SLICED = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe")  # the sliced layout
+_EXACT_KERNELS = ("rowblock", "staged", "scalar", "wstream", "sliced", "sliced_pipe", "tiled")
+_SLICED = ("sliced", "sliced_pipe")  # the sliced layout
 _TREE_KERNELS = ("vector2", "vector4", "vector8", "vector16", "warp")
 GPU_VARIANTS = ("auto", "rowblock_tree") + _EXACT_KERNELS + _TREE_KERNELS
 _CODE_NAME = {v: k for k, v in _native.VARIANT_CODES.items()}

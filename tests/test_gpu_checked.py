@@ -26,7 +26,7 @@ from paper_2307_06305_b200.workloads import add_skew_rows, laplacian_2d, uniform
 from test_oracle import CORPUS
 assert _native.LIB_PATH.endswith("_checked.so"), _native.LIB_PATH
 dev = torch.device("cuda")
-kernels = ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe", "wstream", "rowblock", "staged", "scalar", "vector4", "warp", "rowblock_tree",
+kernels = ("sliced", "sliced_pipe", "tiled", "wstream", "rowblock", "staged", "scalar", "vector4", "warp", "rowblock_tree",
            "multi_accumulator_3", "strip_mined_4")
 for c in CORPUS:
     for kind, inner in (("csr", "colids"), ("da", "offsets")):
@@ -48,9 +48,18 @@ for rows in (32, 64):
         assert np.array_equal(y.cpu().numpy(), ref)
 for max_len, medium_len in ((1, 1), (3, 3), (5, 40), (40, 254)):
     dm.build_slices(max_len, medium_len)
-    for v in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"):
+    for v in ("sliced", "sliced_pipe", "tiled"):
         y = dg.spmv(dm, x, variant=v)
         assert np.array_equal(y.cpu().numpy(), ref)
+for tc in (64, 256, 4096):  # many tiles, left-out rows, partial last tiles
+    dm.build_tiles(tc)
+    y = dg.spmv(dm, x, variant="tiled")
+    assert np.array_equal(y.cpu().numpy(), ref)
+    xe = torch.zeros(a.ncols + 77, dtype=torch.float64, device=dev)
+    xe[37:37 + a.ncols] = x
+    y = torch.full((a.nrows,), 3.0, dtype=torch.float64, device=dev)
+    dm.spmv_into(xe, y, 1.0, 0.0, "tiled", 0, x_offset=37, row_start=700, row_end=9000)
+    assert np.array_equal(y.cpu().numpy()[700:9000], ref[700:9000])
 for v in kernels:
     y = dg.spmv(dm, x, variant=v)
 torch.cuda.synchronize()

@@ -55,19 +55,35 @@ def test_c3_full_size(cuda):
         assert all(vals[i] == oracle.gen_value(b, seed, int(r), int(o), table)
                    for i, o in enumerate(want))
     x = normal_vector(n, 17, cuda)
+    # the row-statistics selection sends this random band to TILED
+    from paper_2307_06305_b200.spmv import kernel_for
+    assert da.stats.scatter > 0.9 and kernel_for(da, "exact", 0) == "tiled"
+    assert kernel_for(csr, "exact", 0) == "tiled"
     yd = dg.spmv(da, x, variant="naive")
     yc = dg.spmv(csr, x, variant="naive")
     assert torch.equal(yd, yc)  # naive CSR == naive DA bit-exact (reference crit 4)
+    # the FULL y against the oracle (the reference's naive kernel restated in
+    # C, all host threads), DA and CSR
+    import os
+    rp = da.rowptr.cpu().numpy()
+    xh = x.cpu().numpy()
+    ref = oracle.spmv("da", rp, da.colids.cpu().numpy(), da.values.cpu().numpy(), xh,
+                      threads=len(os.sched_getaffinity(0)))
+    assert np.array_equal(yd.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+    ref_c = oracle.spmv("csr", rp, csr.colids.cpu().numpy(), csr.values.cpu().numpy(), xh,
+                        threads=len(os.sched_getaffinity(0)))
+    assert np.array_equal(ref_c.view(np.uint64), ref.view(np.uint64))
+    del ref_c
     # every exact kernel (both layouts) gives the same bits at full size
     for dm in (da, csr):
-        for kernel in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe", "wstream", "scalar"):
+        for kernel in ("sliced", "sliced_pipe", "tiled", "wstream", "scalar"):
             yk = torch.empty(n, dtype=torch.float64, device=cuda)
             dm.spmv_into(x, yk, 1.0, 0.0, kernel, 0)
             assert torch.equal(yk, yd), (dm.kind, kernel)
         dm._sliced = None
+        dm._tiled = None
         dm._launch_cache.clear()
     # sampled rows against the oracle kernel on the copied row data
-    xh = x.cpu().numpy()
     yh = yd.cpu().numpy()
     for r, (offs, vals) in zip(rows, _sample_rows(da, rows)):
         rp = np.array([0, len(offs)], np.int64)
@@ -101,7 +117,7 @@ def test_c4_rcm_and_skew(cuda):
     assert info["bandwidth_rcm"] == g["bandwidth_rcm"]
     d = dg.to_dacsr(a, 16)
     x = np.random.default_rng(3).uniform(-1, 1, a.ncols)
-    for variant in ("naive", "strip_mined_4", "sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"):
+    for variant in ("naive", "strip_mined_4", "sliced", "sliced_pipe", "tiled"):
         y = dg.spmv(d, x, variant=variant)
         order = variant if variant in ("naive", "strip_mined_4") else "naive"
         ref = oracle.spmv("da", d.rowptr, d.colids, d.values, x, order=order, threads=8)

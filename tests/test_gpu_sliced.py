@@ -69,7 +69,7 @@ def test_layout_is_a_rearrangement(cuda, kind):
 
 @pytest.mark.parametrize("kind", ["csr", "da"])
 @pytest.mark.parametrize("lens", [None, (1, 1), (1, 3), (3, 40)])
-@pytest.mark.parametrize("variant", ["sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"])
+@pytest.mark.parametrize("variant", ["sliced", "sliced_pipe", "tiled"])
 def test_golden_bit_exact(cuda, kind, lens, variant):
     max_len = lens
     for k, c in enumerate(CORPUS):
@@ -83,7 +83,7 @@ def test_golden_bit_exact(cuda, kind, lens, variant):
         assert np.array_equal(bits(y.cpu().numpy()), bits(c["y_naive"])), (k, kind, max_len)
 
 
-@pytest.mark.parametrize("variant", ["sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"])
+@pytest.mark.parametrize("variant", ["sliced", "sliced_pipe", "tiled"])
 def test_row_ranges_and_x_offset(cuda, variant):
     a = dg.to_dacsr(add_skew_rows(laplacian_2d(96), frac=0.03, alpha=0.3, cap=700, band=500,
                                   seed=4), 16)
@@ -112,20 +112,13 @@ def test_c2_full_size_matches_exact_kernels(cuda, dtype):
     x = torch.from_numpy(uniform_x(a.ncols, 1)).to(cuda).to(dtype)
     want = dm.spmv_into(x, torch.empty(a.nrows, dtype=dtype, device=cuda), 1.0, 0.0, "wstream")
     got = dm.spmv_into(x, torch.empty(a.nrows, dtype=dtype, device=cuda), 1.0, 0.0, "sliced")
-    got2 = dm.spmv_into(x, torch.empty(a.nrows, dtype=dtype, device=cuda), 1.0, 0.0,
-                        "sliced_tma")
-    got3 = dm.spmv_into(x, torch.empty(a.nrows, dtype=dtype, device=cuda), 1.0, 0.0,
-                        "sliced_ring")
-    got4 = dm.spmv_into(x, torch.empty(a.nrows, dtype=dtype, device=cuda), 1.0, 0.0,
-                        "sliced_pred")
     got5 = dm.spmv_into(x, torch.empty(a.nrows, dtype=dtype, device=cuda), 1.0, 0.0,
                         "sliced_pipe")
+    got6 = dm.spmv_into(x, torch.empty(a.nrows, dtype=dtype, device=cuda), 1.0, 0.0, "tiled")
     as_int = {8: torch.int64, 4: torch.int32, 2: torch.int16}[dtype.itemsize]
     assert torch.equal(got.view(as_int), want.view(as_int))
-    assert torch.equal(got2.view(as_int), want.view(as_int))
-    assert torch.equal(got3.view(as_int), want.view(as_int))
-    assert torch.equal(got4.view(as_int), want.view(as_int))
     assert torch.equal(got5.view(as_int), want.view(as_int))
+    assert torch.equal(got6.view(as_int), want.view(as_int))
     if dtype == torch.float64:
         ref = oracle.spmv("da", a.rowptr, a.colids, a.values, x.cpu().numpy())
         assert np.array_equal(bits(got.cpu().numpy()), bits(ref))
@@ -138,7 +131,7 @@ def test_skewed_spill_rows_full_size(cuda):
     dm = DeviceMatrix.of(a)
     x = torch.from_numpy(uniform_x(a.ncols, 2)).to(cuda)
     ref = oracle.spmv("da", a.rowptr, a.colids, a.values, x.cpu().numpy())
-    for variant in ("sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"):
+    for variant in ("sliced", "sliced_pipe", "tiled"):
         got = dm.spmv_into(x, torch.empty(a.nrows, dtype=torch.float64, device=cuda), 1.0, 0.0,
                            variant)
         assert np.array_equal(bits(got.cpu().numpy()), bits(ref)), variant
@@ -146,7 +139,7 @@ def test_skewed_spill_rows_full_size(cuda):
     assert info["n_medium"] > 0 and info["n_long"] > 0
 
 
-@pytest.mark.parametrize("variant", ["sliced", "sliced_tma", "sliced_ring", "sliced_pred", "sliced_pipe"])
+@pytest.mark.parametrize("variant", ["sliced", "sliced_pipe", "tiled"])
 def test_streamed_host_path_on_slices(cuda, variant):
     """spmv(A, x_host, y_host) with the slices: the row pieces of the
     streamed host path share the whole matrix's layout; bit-exact."""
@@ -179,7 +172,7 @@ def test_l2_prefetch_flag_keeps_bits(cuda):
     ref = oracle.spmv("da", a.rowptr, a.colids, a.values, x.cpu().numpy())
     for on in (False, True):
         dm.set_sliced_l2_prefetch(on)
-        for variant in ("sliced", "sliced_pipe", "sliced_pred"):
+        for variant in ("sliced", "sliced_pipe"):
             y = dm.spmv_into(x, torch.empty(a.nrows, dtype=torch.float64, device=cuda), 1.0,
                              0.0, variant)
             assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (on, variant)

@@ -1,0 +1,155 @@
+"""The band-tiled device layout (dacsr_tiles_t) and the TILED kernel — needs a B200.
+
+The layout is a bit-for-bit re-arrangement of the CSR/DA-CSR entries (512-row
+groups, column tiles, pair-step packed lane lists); the kernel folds every
+row from +0.0 in column order, i.e. the reference's naive order
+(_numba_kernels.py:82-91), so every result here is BIT-EXACT against the
+reference outputs (tests/golden) and the oracle.  Rows with more than 15
+entries inside one tile are left out of the layout and reduced warp by warp;
+small tile widths force that path, many tiles per group and partial tiles.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2307_06305_b200 as dg
+from paper_2307_06305_b200.device import DeviceMatrix
+from paper_2307_06305_b200.gen import banded_arrays, normal_vector
+from paper_2307_06305_b200.workloads import add_skew_rows, laplacian_2d, uniform_x
+from test_gpu_parity import bits, host_matrix
+from test_oracle import CORPUS
+
+pytestmark = pytest.mark.gpu
+
+
+def untile(dm):
+    """Decode the layout: {row: [(tile, inner, value), ...]} in storage order,
+    the skip masks and the left-out row list."""
+    _, tl, t = dm._tiled
+    ptrs = t["ptrs"].cpu().numpy()
+    cnt_ptr, ent_ptr = ptrs[0], ptrs[1]
+    tile_lo = t["tile_lo"].cpu().numpy()
+    counts = t["counts"].cpu().numpy().view(np.uint64)
+    inner, vals = t["inner"].cpu().numpy(), t["values"].cpu().numpy()
+    rows = {}
+    for g in range(tl.ngroups):
+        pos = int(ent_ptr[g])
+        for k in range(int(cnt_ptr[g + 1] - cnt_ptr[g])):
+            nib = counts[(cnt_ptr[g] + k) * 32:(cnt_ptr[g] + k + 1) * 32]
+            n = [[(int(nib[l]) >> (4 * j)) & 15 for j in range(16)] for l in range(32)]
+            tot = [sum(v) for v in n]
+            lists = [[] for _ in range(32)]
+            for q in range((max(tot) + 1) // 2):
+                for l in range(32):
+                    if 2 * q < tot[l]:
+                        lists[l] += [pos, pos + 1]
+                        pos += 2
+            for l in range(32):
+                slots = iter(lists[l])
+                for j in range(16):
+                    r = tl.row_start + 512 * g + 32 * j + l
+                    for _ in range(n[l][j]):
+                        p = next(slots)
+                        rows.setdefault(r, []).append((int(tile_lo[g]) + k, inner[p], vals[p]))
+        assert pos == ent_ptr[g + 1]
+    skip = t["skip"].cpu().numpy().view(np.uint16)
+    return rows, skip, t["ovf_rows"].cpu().numpy()[:tl.n_ovf]
+
+
+@pytest.mark.parametrize("kind", ["csr", "da"])
+def test_layout_is_a_rearrangement(cuda, kind):
+    for c in CORPUS[::5]:
+        a = host_matrix(c, kind)
+        dm = DeviceMatrix.from_host(a, cuda)
+        rp = np.asarray(a.rowptr, dtype=np.int64)
+        for tc in (64, 128, 8192):
+            dm.build_tiles(tc)
+            tl = dm._tiled[1]
+            rows, skip, ovf = untile(dm)
+            assert list(ovf) == sorted(ovf)
+            assert not set(rows) & set(int(r) for r in ovf)
+            for r in range(a.nrows):
+                b, e = rp[r], rp[r + 1]
+                if r in set(int(v) for v in ovf):
+                    continue
+                got = rows.get(r, [])
+                assert len(got) == e - b, (r, tc)
+                cols = np.asarray(a.colids)[b:e].astype(np.int64) + (r if kind == "da" else 0)
+                for i, (tile, inn, val) in enumerate(got):
+                    assert inn == np.asarray(a.colids)[b + i]
+                    assert bits(np.array([val])) .tobytes() == bits(np.asarray(a.values)[b + i:b + i + 1]).tobytes()
+                    assert tile == (cols[i] - tl.col0) // tc
+
+
+@pytest.mark.parametrize("kind", ["csr", "da"])
+@pytest.mark.parametrize("tile_cols", [None, 64, 256])
+def test_golden_bit_exact(cuda, kind, tile_cols):
+    for k, c in enumerate(CORPUS):
+        dm = DeviceMatrix.from_host(host_matrix(c, kind), cuda)
+        dm.build_tiles(tile_cols)
+        x = torch.from_numpy(c["x"]).to(cuda)
+        y = torch.from_numpy(c["y0"].copy()).to(cuda)
+        out = dg.spmv(dm, x, y, c["alpha"], c["beta"], "tiled")
+        assert out is y
+        assert np.array_equal(bits(y.cpu().numpy()), bits(c["y_naive"])), (k, kind, tile_cols)
+
+
+@pytest.mark.parametrize("kind", ["csr", "da"])
+def test_wide_band_left_out_rows_ranges_x_offset(cuda, kind):
+    """Random band (C3 shape, small n): tiny tiles leave rows out; every row
+    range and a rank-local halo buffer (x_offset) stay bit-exact."""
+    n, b = 1 << 14, 3000
+    arr = banded_arrays(n, b, 16.0, 64, 5, cuda, kinds=("da", "csr"))
+    rp = arr["rowptr"].cpu().numpy()
+    offs = arr["offsets"].cpu().numpy()
+    vals = arr["values"].cpu().numpy()
+    dm = DeviceMatrix(kind, n, n, arr["rowptr"], arr["offsets" if kind == "da" else "colids"],
+                      arr["values"])
+    xh = normal_vector(n, 3, cuda).cpu().numpy()
+    pad = 41
+    x_ext = torch.zeros(n + 2 * pad, dtype=torch.float64, device=cuda)
+    x_ext[pad:pad + n] = torch.from_numpy(xh).to(cuda)
+    rng = np.random.default_rng(4)
+    for tc in (4096, 6000 // 16 * 16):
+        dm.build_tiles(tc)
+        assert dm.tiles_info()["n_ovf"] > 0
+        for _ in range(6):
+            r0, r1 = sorted(int(v) for v in rng.integers(0, n + 1, 2))
+            y0 = rng.uniform(-1, 1, n)
+            y = torch.from_numpy(y0.copy()).to(cuda)
+            dm.spmv_into(x_ext, y, 0.7, -0.3, "tiled", 0, x_offset=pad, row_start=r0, row_end=r1)
+            ref = oracle.spmv_kernel("da", rp, offs, vals, xh, y0.copy(), 0.7, -0.3,
+                                     row_start=r0, row_end=r1)
+            assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (tc, r0, r1)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+def test_narrow_values_match_exact_kernels(cuda, dtype):
+    n = 1 << 15
+    arr = banded_arrays(n, 32767, 8.0, 32, 6, cuda, kinds=("da",))
+    dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"]).astype(dtype)
+    x = normal_vector(n, 9, cuda).to(dtype)
+    want = dm.spmv_into(x, torch.empty(n, dtype=dtype, device=cuda), 1.0, 0.0, "scalar")
+    got = dm.spmv_into(x, torch.empty(n, dtype=dtype, device=cuda), 1.0, 0.0, "tiled")
+    as_int = {4: torch.int32, 2: torch.int16}[dtype.itemsize]
+    assert torch.equal(got.view(as_int), want.view(as_int))
+    assert dm.tiles_info()["tile_cols"] == 65536 // dtype.itemsize
+
+
+def test_skewed_rows_and_default_selection(cuda):
+    """Skewed stencil (C4-like): the tiled kernel stays exact with long rows
+    left out; the default selection keeps SLICED_PIPE for it."""
+    a = dg.to_dacsr(add_skew_rows(laplacian_2d(256), frac=0.02, alpha=0.5, cap=1200, band=700,
+                                  seed=3), 16)
+    dm = DeviceMatrix.from_host(a, cuda)
+    x = torch.from_numpy(uniform_x(a.ncols, 5)).to(cuda)
+    ref = oracle.spmv("da", a.rowptr, a.colids, a.values, x.cpu().numpy())
+    for tc in (64, 1024, 8192):
+        dm.build_tiles(tc)
+        y = dg.spmv(dm, x, variant="tiled")
+        assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), tc
+    assert dm.stats.scatter < 0.5
+    from paper_2307_06305_b200.spmv import kernel_for
+    assert kernel_for(dm, "exact", 0) == "sliced_pipe"
