@@ -322,13 +322,19 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
   uint32_t rph = 0;
   ChunkMeta nq = load_meta(blockIdx.x);
   // this warp's group's first two count words, loaded a chunk ahead too
+  // the operator segment of a tile: its lanes' lists rounded up to pairs
+  auto seg_slots = [&](uint64_t w) {
+    return static_cast<int>(
+        __reduce_add_sync(0xffffffffu, static_cast<unsigned>((nibble_sum(w) + 1) & ~1)));
+  };
   uint64_t ncn0 = 0, ncn1 = 0;
-  {
-    const int64_t c0 = __shfl_sync(0xffffffffu, nq.cnt0, warp);
-    const int64_t c1 = __shfl_sync(0xffffffffu, nq.cnt1, warp);
-    if (c1 > c0) ncn0 = ldg(ta.counts + c0 * 32 + lane);
-    if (c1 > c0 + 1) ncn1 = ldg(ta.counts + (c0 + 1) * 32 + lane);
-  }
+  auto load_first_counts = [&](const ChunkMeta& q2) {
+    const int64_t c0 = __shfl_sync(0xffffffffu, q2.cnt0, warp);
+    const int64_t c1 = __shfl_sync(0xffffffffu, q2.cnt1, warp);
+    ncn0 = c1 > c0 ? ldg(ta.counts + c0 * 32 + lane) : 0;
+    ncn1 = c1 > c0 + 1 ? ldg(ta.counts + (c0 + 1) * 32 + lane) : 0;
+  };
+  load_first_counts(nq);
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const ChunkMeta q = nq;
     nq = load_meta(c + gridDim.x);
@@ -343,31 +349,34 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
 #pragma unroll
     for (int j = 0; j < kTileRows; ++j) sts_f64(wa + 256u * j, 0.0);
     uint64_t cn0 = ncn0, cn1 = ncn1;
-    if (gnt > 0)
-      prefetch_segment(pos, __reduce_add_sync(0xffffffffu, static_cast<unsigned>(nibble_sum(cn0))));
+    // the operator segment of the group's first tile into L2 now, every
+    // later one a tile ahead of its fold (bulk prefetch; measured: without
+    // it C3 runs 11 % slower, two tiles ahead 4 % slower)
+    int64_t pf_pos = pos;
+    if (gnt > 0) {
+      const int n0 = seg_slots(cn0);
+      prefetch_segment(pf_pos, n0);
+      pf_pos += n0;
+    }
     // rows of lane l: row0 + 512g + 32j + l
     const int64_t lrow = ta.row0 + 512 * g + lane;
     for (int64_t t = tlo; t <= thi; ++t) {
       const int64_t k = t - gtlo;
       const bool mine = has && k >= 0 && k < gnt;
       uint64_t cur = 0;
-      int total = 0, here = 0;
+      int total = 0;
       if (mine) {
         cur = cn0;
         cn0 = cn1;
         cn1 = k + 2 < gnt ? ldg(ta.counts + (cbase + k + 2) * 32 + lane) : 0;
         total = nibble_sum(cur);
-        here = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(total)));
-        if (k + 1 < gnt)
-          prefetch_segment(pos + here,
-                           __reduce_add_sync(0xffffffffu, static_cast<unsigned>(nibble_sum(cn0))));
+        if (k + 1 < gnt) {
+          const int n = seg_slots(cn0);
+          prefetch_segment(pf_pos, n);
+          pf_pos += n;
+        }
       }
-      if (t == thi) {  // the next chunk's first count words
-        const int64_t c0 = __shfl_sync(0xffffffffu, nq.cnt0, warp);
-        const int64_t c1 = __shfl_sync(0xffffffffu, nq.cnt1, warp);
-        ncn0 = c1 > c0 ? ldg(ta.counts + c0 * 32 + lane) : 0;
-        ncn1 = c1 > c0 + 1 ? ldg(ta.counts + (c0 + 1) * 32 + lane) : 0;
-      }
+      if (t == thi) load_first_counts(nq);  // the next chunk's first count words
       mbar_wait_sleep(&full[rb], rph);
       if (mine) {
         const int64_t cs = ta.col0 + t * ta.T;

@@ -130,19 +130,29 @@ def exchange_halo(x_ext, plan, group=None):
     return dist.batch_isend_irecv(ops)
 
 
-def gather_partials(p, group=None):
-    """All ranks' chunk partials concatenated in rank order."""
+def gather_partials(p, group=None, counts=None):
+    """All ranks' chunk partials concatenated in rank order.  With the
+    per-rank ``counts`` known (they follow from the partition) this is one
+    fixed-size all_gather; otherwise the counts are exchanged first."""
     world = dist.get_world_size(group)
-    count = torch.tensor([p.numel()], dtype=torch.int64, device=p.device)
-    counts = [torch.zeros_like(count) for _ in range(world)]
-    dist.all_gather(counts, count, group=group)
-    counts = [int(c.item()) for c in counts]
+    if counts is None:
+        count = torch.tensor([p.numel()], dtype=torch.int64, device=p.device)
+        cs = [torch.zeros_like(count) for _ in range(world)]
+        dist.all_gather(cs, count, group=group)
+        counts = [int(c.item()) for c in cs]
     m = max(counts)
-    padded = torch.zeros(m, dtype=p.dtype, device=p.device)
-    padded[:p.numel()] = p
-    bufs = [torch.empty_like(padded) for _ in range(world)]
-    dist.all_gather(bufs, padded, group=group)
-    return torch.cat([b[:c] for b, c in zip(bufs, counts)])
+    padded = p if p.numel() == m else torch.cat(
+        [p, torch.zeros(m - p.numel(), dtype=p.dtype, device=p.device)])
+    out = torch.empty(world * m, dtype=p.dtype, device=p.device)
+    dist.all_gather_into_tensor(out, padded.contiguous(), group=group)
+    if all(c == m for c in counts):
+        return out
+    return torch.cat([out[q * m:q * m + c] for q, c in enumerate(counts)])
+
+
+def chunk_counts(part, chunk):
+    """Norm-chunk partials per rank (rank boundaries on chunk multiples)."""
+    return [-(-(b - a) // chunk) for a, b in part.bounds]
 
 
 class CudaLocalOp:
@@ -163,9 +173,15 @@ class CudaLocalOp:
         name, order = resolve_variant(variant)
         self.order = order
         self.mats = []
+        full = None
+        if name == "exact" and n_local:
+            # the library's selection on this rank's rows (row statistics)
+            full = DeviceMatrix(kind, n_local, ncols_global, rowptr, colids, values)
+            name = kernel_for(full, name, order)
         if name in LAYOUT_KERNELS and n_local:
             # one derived layout of all local rows serves the three row ranges
-            full = DeviceMatrix(kind, n_local, ncols_global, rowptr, colids, values)
+            if full is None:
+                full = DeviceMatrix(kind, n_local, ncols_global, rowptr, colids, values)
             full.build_tiles() if name == "tiled" else full.build_slices()
             self.mats = [full if r1 > r0 else None for r0, r1 in self.ranges]
             self.kernels = [name if r1 > r0 else None for r0, r1 in self.ranges]
@@ -223,23 +239,25 @@ def dist_spmv(op, x_ext, y, alpha, plan, group=None, overlap=True):
     return y
 
 
-def power_iteration(op, plan, x0_own, iters, group=None, overlap=True):
+def power_iteration(op, plan, x0_own, iters, group=None, overlap=True, counts=None):
     """Distributed normalised power iteration from x0 (this rank's rows).
 
     Returns (x_own, norms): x_own = x_iters restricted to this rank's rows,
-    norms[k] = ||A x_k||.  Identical bits for every rank count.
+    norms[k] = ||A x_k||.  Identical bits for every rank count.  ``counts``:
+    the per-rank number of norm chunks (chunk_counts), which makes each norm
+    one fixed-size all_gather.
     """
     dev = x0_own.device
     bufs = [torch.zeros(plan.length, dtype=x0_own.dtype, device=dev) for _ in range(2)]
     own = plan.own_slice()
     bufs[0][own] = x0_own
-    s_prev = math.sqrt(op.fold(gather_partials(op.partials(x0_own), group)))
+    s_prev = math.sqrt(op.fold(gather_partials(op.partials(x0_own), group, counts)))
     norms = []
     cur = 0
     for _ in range(iters):
         nxt = 1 - cur
         dist_spmv(op, bufs[cur], bufs[nxt][own], 1.0 / s_prev, plan, group, overlap)
-        s_prev = math.sqrt(op.fold(gather_partials(op.partials(bufs[nxt][own]), group)))
+        s_prev = math.sqrt(op.fold(gather_partials(op.partials(bufs[nxt][own]), group, counts)))
         norms.append(s_prev)
         cur = nxt
     x = bufs[cur][own].clone()
@@ -257,27 +275,6 @@ def _scale_device(x, s):
 
 
 # ------------------------------------------------------------------ bench
-def slab_laplacian_3d(nx, nz_total, z0, z1, dtype=np.float64):
-    """Rows of planes [z0, z1) of the nx*nx*nz_total 7-point Laplacian
-    (global columns), canonical CSR; the weak-scaling slab of one rank."""
-    from .workloads import _stencil_csr
-    full = None
-    # build the slab with one ghost plane each side, then keep its rows
-    g0, g1 = max(0, z0 - 1), min(nz_total, z1 + 1)
-    st = [(0, -1), (1, -1), (2, -1), (0, 0), (2, 1), (1, 1), (0, 1)]
-    sub = _stencil_csr((g1 - g0, nx, nx), st, 6.0, -1.0, dtype)
-    plane = nx * nx
-    r_lo, r_hi = (z0 - g0) * plane, (z1 - g0) * plane
-    rp = sub.rowptr.astype(np.int64)
-    e0, e1 = int(rp[r_lo]), int(rp[r_hi])
-    colids = sub.colids[e0:e1].astype(np.int64) + g0 * plane
-    rowptr = (rp[r_lo:r_hi + 1] - e0)
-    # rows on the true global boundary planes are already correct; interior
-    # slab faces had their ghost neighbours included via the ghost planes
-    del full
-    return rowptr.astype(np.int32), colids, sub.values[e0:e1]
-
-
 def _peak_gbs():
     import json
     import os
@@ -290,94 +287,65 @@ def _peak_gbs():
         return 6650.0
 
 
+def iterate_digest(x_own, r0, chunk, group=None):
+    """Partition-independent SHA-256 of the global iterate: per-chunk digests
+    of this rank's rows (rank boundaries are chunk multiples), gathered in
+    chunk order on every rank, hashed once more."""
+    import hashlib
+    xh = x_own.cpu().numpy()
+    digs = [hashlib.sha256(xh[i:i + chunk].tobytes()).digest() for i in range(0, len(xh), chunk)]
+    mine = torch.tensor(np.frombuffer(b"".join(digs), dtype=np.uint8).copy())
+    world = dist.get_world_size(group)
+    sizes = [None] * world
+    dist.all_gather_object(sizes, (r0, mine.numel()), group=group)
+    allb = [None] * world
+    dist.all_gather_object(allb, bytes(mine.numpy()), group=group)
+    order = sorted(range(world), key=lambda q: sizes[q][0])
+    return hashlib.sha256(b"".join(allb[q] for q in order)).hexdigest()
+
+
 def bench_main(args, rank, world, local):
-    """Weak scaling: rank p owns planes [128p, 128p+128) of a 128x128x(128N)
-    Laplacian (C2 per rank), DA-CSR f64; a step = 100 distributed SpMVs
-    (halo exchange + interior/boundary kernels), power-iteration style."""
+    """Config C5 at N ranks (strong scaling): 50 normalised power iterations
+    x <- A x / ||A x|| on the 2^28-row band (b = 32767, clip(Poisson(8), 1,
+    32), DA-CSR i16, f64).  Rows in equal contiguous blocks aligned to the
+    2^16-row norm chunk; each rank generates its rows on its GPU (identical
+    to the same rows of the whole matrix), runs the library's default kernel
+    for them (row statistics -> TILED) with the +-b halo exchanged over NCCL
+    while the interior rows run, and folds the norm from one fixed-size
+    all_gather of chunk partials.  One step = the 50 iterations; max over
+    ranks of CUDA-event step times."""
     import json
     import time
+    from .gen import banded_arrays, normal_vector
     from .harness import ClockSampler
     from .model import StorageWidths, spmv_traffic
+    from .workloads import BANDED_CONFIGS
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    nx = 128
-    plane = nx * nx
-    n = plane * nx * world
-    part = RowPartition(n, tuple((p * plane * nx, (p + 1) * plane * nx) for p in range(world)))
-    plan = halo_plan(part, rank, plane)
-    rp, cols, vals = slab_laplacian_3d(nx, nx * world, rank * nx, (rank + 1) * nx)
-    r0 = part.bounds[rank][0]
-    rows = np.repeat(np.arange(len(rp) - 1, dtype=np.int64), np.diff(rp)) + r0
-    offs = (cols - rows).astype(np.int16)
-    t_rp = torch.from_numpy(rp).to(dev)
-    t_off = torch.from_numpy(offs).to(dev)
-    t_val = torch.from_numpy(np.ascontiguousarray(vals)).to(dev)
-    x = torch.from_numpy(np.random.default_rng(1 + rank).uniform(-1, 1, len(rp) - 1)).to(dev)
-    bufs = [torch.zeros(plan.length, dtype=torch.float64, device=dev) for _ in range(2)]
-    own = plan.own_slice()
-    bufs[0][own] = x
-    # the exact kernels give the same bits: time each on the real distributed
-    # step (max over ranks) and keep the fastest everywhere
-    # (graph capture of NCCL P2P is only attempted at one rank here: a failed
-    # capture on a multi-rank communicator is not worth the risk before the
-    # timed run; at N > 1 the kernel measured fastest at one rank is used)
-    tuned = {}
-    for cand in (("sliced_pipe", "sliced", "wstream") if world == 1 else ("sliced_pipe",)):
-        op = CudaLocalOp("da", t_rp, t_off, t_val, n, plan, 1 << 16, plane, variant=cand)
-        def burst(op=op):
-            for _ in range(20):
-                dist_spmv(op, bufs[0], bufs[1][own], 0.125, plan)
-        burst()
-        torch.cuda.synchronize()
-        run_c = burst
-        try:  # time the graphed form when NCCL P2P can be captured (as timed below)
-            g_c = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g_c):
-                burst()
-            g_c.replay()
-            torch.cuda.synchronize()
-            run_c = g_c.replay
-        except Exception:
-            torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        run_c()
-        e1.record()
-        e1.synchronize()
-        t_c = torch.tensor([e0.elapsed_time(e1) / 20], dtype=torch.float64, device=dev)
-        dist.all_reduce(t_c, op=dist.ReduceOp.MAX)
-        tuned[cand] = round(float(t_c.item()) * 1e3, 2)
-    best = min(tuned, key=tuned.get)
-    op = CudaLocalOp("da", t_rp, t_off, t_val, n, plan, 1 << 16, plane, variant=best)
-    nloc = len(rp) - 1
-    traffic = spmv_traffic(nloc, nloc, len(offs), StorageWidths(4, 2, 8)).total_bytes
-
-    def step():
-        cur = 0
-        for _ in range(100):
-            dist_spmv(op, bufs[cur], bufs[1 - cur][own], 0.125, plan)
-            cur = 1 - cur
-
-    for _ in range(max(1, args.warmup)):
-        step()
+    n, b, lam, kmax, seed = BANDED_CONFIGS["c5"]
+    chunk = 1 << 16
+    iters = 50
+    part = RowPartition.equal(n, world, align=chunk)
+    plan = halo_plan(part, rank, b)
+    counts = chunk_counts(part, chunk)
+    r0, r1 = part.bounds[rank]
+    t0 = time.time()
+    arr = banded_arrays(n, b, lam, kmax, seed, dev, r0=r0, r1=r1, kinds=("da",))
+    op = CudaLocalOp("da", arr["rowptr"], arr["offsets"], arr["values"], n, plan, chunk, b)
+    x0 = normal_vector(r1 - r0, 21, dev, i0=r0)
     torch.cuda.synchronize()
-    # capture the 100-SpMV step (kernels + NCCL halo P2P) in one CUDA graph;
-    # eager launches are host-bound at ~3 launches per 31 us SpMV
-    run, graphed = step, False
-    try:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            step()
-        g.replay()
-        torch.cuda.synchronize()
-        run, graphed = g.replay, True
-    except Exception as exc:  # NCCL P2P capture unsupported: stay eager
-        import sys
-        print(f"[rank {rank}] graph capture failed ({type(exc).__name__}: {exc}); eager",
-              file=sys.stderr, flush=True)
+    build_s = time.time() - t0
+    nnz_local = torch.tensor([arr["nnz"]], dtype=torch.int64, device=dev)
+    dist.all_reduce(nnz_local)
+    nnz = int(nnz_local.item())
+    # whole-job algorithmic bytes per SpMV: the 1-GPU model of the whole
+    # matrix (rowptr counted at int32, as every rank stores it)
+    traffic = spmv_traffic(n, n, nnz, StorageWidths(4, 2, 8)).total_bytes
+    for _ in range(max(1, args.warmup)):
+        power_iteration(op, plan, x0, 2, counts=counts)
+    torch.cuda.synchronize()
     dist.barrier()
     times = []
     with ClockSampler(local) as clocks:
@@ -387,58 +355,63 @@ def bench_main(args, rank, world, local):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            run()
+            x, norms = power_iteration(op, plan, x0, iters, counts=counts)
             e1.record()
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
     t = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total = float(t.item())
-    value = world * args.steps * 100 * traffic / total / 1e9
+    step = total / args.steps
+    value = iters * traffic / step / 1e9
+    digest = iterate_digest(x, r0, chunk)
 
-    # e2e: host buffers through the same path — every SpMV copies this rank's
-    # x rows in (pinned) and its y rows out; 10 SpMVs per step, max over ranks
-    e2e_spmv = 10
-    xh = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
-    yh = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
-    xh.copy_(x.cpu())
-    e2e_steps = max(2, args.steps // 5)
+    # e2e: host buffers through the same path — every SpMV copies this
+    # rank's x rows in from pinned memory and its y rows out; max over ranks
+    e2e_spmv, e2e_steps = 2, 2
+    own = plan.own_slice()
+    bufs = [torch.zeros(plan.length, dtype=torch.float64, device=dev) for _ in range(2)]
+    xh = torch.empty(r1 - r0, dtype=torch.float64, pin_memory=True)
+    yh = torch.empty(r1 - r0, dtype=torch.float64, pin_memory=True)
+    xh.copy_(x0.cpu())
     dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    tt = time.perf_counter()
     for _ in range(e2e_steps):
         for _ in range(e2e_spmv):
             bufs[0][own].copy_(xh, non_blocking=True)
             dist_spmv(op, bufs[0], bufs[1][own], 1.0, plan)
             yh.copy_(bufs[1][own], non_blocking=True)
             torch.cuda.current_stream().synchronize()
-    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    el = torch.tensor([time.perf_counter() - tt], dtype=torch.float64, device=dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    e2e_gbs = world * e2e_steps * e2e_spmv * traffic / float(el.item()) / 1e9
+    e2e_gbs = e2e_steps * e2e_spmv * traffic / float(el.item()) / 1e9
     if rank == 0:
         line = {
             "metric": "SpMV effective HBM GB/s (DA-CSR i16, f64)", "value": round(value, 1),
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 * total / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2 per rank: 128x128x(128*{world}) 7-pt Laplacian slabs, "
-                                   "DA-CSR i16 f64, +-16384-row halo exchange (NCCL "
-                                   "send/recv) overlapped with interior rows",
-                       "spmv_per_step": 100, "parallelism": f"row blocks x{world}",
-                       "cuda_graph": graphed, "kernel": best,
-                       "kernel_selection": "fastest exact kernel on the distributed step, "
-                                           "us per SpMV (20 graphed, max over ranks): "
-                                           + json.dumps(tuned)},
+            "ms_per_step": round(1e3 * step, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5: 50 normalised power iterations, banded n=2^28, b=32767, "
+                                   "clip(Poisson(8),1,32), DA-CSR i16 f64",
+                       "nnz": nnz, "bytes_per_spmv": traffic, "iters_per_step": iters,
+                       "parallelism": f"row blocks x{world}, +-{b}-row halo (NCCL send/recv "
+                                      "overlapped with the interior rows), norm: one "
+                                      "all_gather of 2^16-row chunk partials",
+                       "kernel": op.kernels[0], "build_s": round(build_s, 1),
+                       "final_norm": norms[-1],
+                       "iterate_sha256": digest,
+                       "note": "final_norm and iterate_sha256 are identical for every rank "
+                               "count (deterministic chunked norm)"},
             "roofline": {"bound": "hbm", "achieved": round(value / world, 1),
                          "peak": _peak_gbs(), "unit": "GB/s",
                          "frac": round(value / world / _peak_gbs(), 4), "traffic": None,
-                         "note": "per GPU: local slab traffic / max-over-ranks step time"},
+                         "note": "per GPU: whole-job model bytes / N / max-over-ranks step time"},
             "e2e": {"value": round(e2e_gbs, 1), "unit": "GB/s",
-                    "h2d_bytes_per_step": world * e2e_spmv * nloc * 8,
-                    "d2h_bytes_per_step": world * e2e_spmv * nloc * 8,
+                    "h2d_bytes_per_step": e2e_spmv * n * 8, "d2h_bytes_per_step": e2e_spmv * n * 8,
                     "spmv_per_step": e2e_spmv,
                     "note": "each rank: pinned host x rows -> distributed SpMV -> host y rows"},
-            "gpu_launches": args.steps * 100 * 3,
+            "gpu_launches": args.steps * iters * 5,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -43,17 +43,27 @@ def fold_ordered(partials, stream=None, out=None):
 
 
 def chunked_sumsq(y, chunk=DEFAULT_CHUNK, stream=None):
-    return float(fold_ordered(chunk_partials(y, chunk, stream), stream).item())
+    out = fold_ordered(chunk_partials(y, chunk, stream), stream)
+    if stream is not None:
+        stream.synchronize()  # .item() reads on the current stream
+    return float(out.item())
 
 
-def power_iteration(dm, x0, iters=50, chunk=DEFAULT_CHUNK, variant="rowblock", order=0,
+def power_iteration(dm, x0, iters=50, chunk=DEFAULT_CHUNK, variant="naive", order=0,
                     stream=None):
     """Run ``iters`` normalised power steps from x0 (device tensor).
+
+    ``variant``: a kernel name, or a reference variant name ("naive", ...)
+    resolved by the library's selection for this matrix.
 
     Returns (x, norms) with norms[k] = ||A x_k|| and x = x_iters.
     x_0 = x0 / ||x0||; y_k = alpha_k * A y_{k-1} with alpha_k = 1/s_{k-1}
     (alpha_0 = 1/||x0||, y_{-1} = x0); s_k = ||y_k||; x_iters = y/s.
     """
+    from .spmv import _EXACT, kernel_for, resolve_variant
+    if variant in _EXACT or variant == "auto":
+        name, order = resolve_variant(variant)
+        variant = kernel_for(dm, name, order)
     bufs = [x0.clone(), torch.empty_like(x0)]
     s_prev = math.sqrt(chunked_sumsq(x0, chunk, stream))
     norms = []

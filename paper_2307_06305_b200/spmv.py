@@ -24,6 +24,7 @@ Host numpy x/y are copied to/from the device inside the call (pinned host
 memory gives async DMA); torch CUDA tensors stay on the device.
 """
 
+import contextlib
 import os
 from dataclasses import dataclass
 
@@ -210,7 +211,11 @@ def spmv(a, x, y=None, alpha=1.0, beta=0.0, variant="naive", backend=None, *, st
     if isinstance(y, torch.Tensor) and not y.is_contiguous():
         raise ValueError("y must be contiguous")
 
-    with torch.cuda.device(dev):
+    # a caller-supplied stream becomes the current stream for the whole call:
+    # host->device copies, the kernel and the device->host copy are then
+    # ordered on it (and temporaries are allocated on it)
+    stream_ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with torch.cuda.device(dev), stream_ctx:
         y_dev = y if isinstance(y, torch.Tensor) else None
         if alpha == 0.0:
             # matrix and x untouched (reference 150-156); y = beta*y on device
@@ -221,7 +226,7 @@ def spmv(a, x, y=None, alpha=1.0, beta=0.0, variant="naive", backend=None, *, st
                          else _to_device(y, dev))
             _native.check(_native.lib().dacsr_scale(
                 _native.ctypes.c_void_p(y_dev.data_ptr()), _native.dtype_code(dm.values.dtype),
-                nrows, beta, _stream_ptr(stream)), "dacsr_scale")
+                nrows, beta, _stream_ptr(None)), "dacsr_scale")
         elif (not isinstance(x, torch.Tensor) and not isinstance(y, torch.Tensor)
               and nrows >= STREAMED_MIN_ROWS and dm.nnz and stream is None):
             # host in, host out: x streams in by row pieces while earlier
@@ -237,13 +242,12 @@ def spmv(a, x, y=None, alpha=1.0, beta=0.0, variant="naive", backend=None, *, st
                 y_dev = (torch.empty(nrows, dtype=dm.values.dtype, device=dev) if beta == 0.0
                          else _to_device(y, dev))
             if nrows:
-                dm.spmv_into(x_dev if ncols else None, y_dev, alpha, beta, kname, order,
-                             stream=stream)
+                dm.spmv_into(x_dev if ncols else None, y_dev, alpha, beta, kname, order)
         if not isinstance(y, torch.Tensor) and nrows:
             out = torch.from_numpy(y)
             out.copy_(y_dev, non_blocking=out.is_pinned())
             if out.is_pinned():
-                (stream or torch.cuda.current_stream()).synchronize()
+                torch.cuda.current_stream().synchronize()
     return y
 
 

@@ -81,7 +81,10 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         plan, op, x0 = _local_problem(rank, world)
-        x, norms = D.power_iteration(op, plan, x0, ITERS, overlap=False)
+        part = D.RowPartition.equal(N, world, align=CHUNK)
+        # world 1 exchanges the counts, world 2 uses the partition's (both paths)
+        counts = D.chunk_counts(part, CHUNK) if world > 1 else None
+        x, norms = D.power_iteration(op, plan, x0, ITERS, overlap=False, counts=counts)
         np.save(f"{out}/x{rank}.npy", x.numpy())
         np.save(f"{out}/norms{rank}.npy", np.array(norms))
     finally:

@@ -27,7 +27,7 @@ def test_sumsq_matches_oracle_restatement(cuda):
     assert float(fold_ordered(p).item()) == oracle.fold_ordered(want)
 
 
-@pytest.mark.parametrize("variant", ["naive", "sliced", "sliced_pipe"])
+@pytest.mark.parametrize("variant", ["naive", "sliced", "sliced_pipe", "tiled"])
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_rank_local_blocks_bit_exact(cuda, world, variant):
     arr = banded_arrays(N, B, LAM, KMAX, SEED, cuda, kinds=("da", "csr"))
@@ -70,31 +70,58 @@ def test_power_iteration_matches_oracle(cuda):
     assert np.array_equal(x.cpu().numpy().view(np.uint64), (xr * (1.0 / s)).view(np.uint64))
 
 
-def test_c5_full_size_sampled(cuda):
-    """Config C5 on one GPU: 2^28 rows, ~2.1e9 entries, int64 rowptr."""
+def test_c5_full_size_row_blocks(cuda):
+    """Config C5 on one GPU (2^28 rows, ~2.1e9 entries) with the default
+    kernel: four contiguous 2^20-row blocks of y (first, last, two interior)
+    bit-exact against the oracle on the same rows (host generator)."""
+    import os
     n, b, lam, kmax, seed = BANDED_CONFIGS["c5"]
     arr = banded_arrays(n, b, lam, kmax, seed, cuda, kinds=("da",))
     # nnz = 2,147,462,688 for this seed: just under 2^31, so rowptr stays int32
     assert arr["nnz"] > 2_000_000_000
     assert arr["rowptr"].dtype == (torch.int64 if arr["nnz"] > 2**31 - 1 else torch.int32)
     dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"])
+    from paper_2307_06305_b200.spmv import kernel_for
+    kernel = kernel_for(dm, "exact", 0)
+    assert kernel == "tiled"
     x = normal_vector(n, 21, cuda)
     y = torch.empty(n, dtype=torch.float64, device=cuda)
-    dm.spmv_into(x, y, 1.0, 0.0, "wstream")
+    dm.spmv_into(x, y, 1.0, 0.0, kernel, 0)
+    del arr, dm
     cdf, table = poisson_cdf(lam, kmax), normal_table()
-    rng = np.random.default_rng(1)
-    rows = np.concatenate([[0, n - 1], rng.integers(0, n, 200)])
-    for r in rows.tolist():
-        offs = oracle.gen_row(n, b, kmax, seed, cdf, r)
-        cols = r + offs.astype(np.int64)
-        vals = np.array([oracle.gen_value(b, seed, r, o, table) for o in offs])
-        xs = oracle.gen_normal(21, 0, 1, table)  # warm the table path
-        xv = np.array([oracle.gen_normal(21, int(c), int(c) + 1, table)[0] for c in cols])
-        acc = 0.0
-        for v, xc in zip(vals.tolist(), xv.tolist()):
-            acc = acc + v * xc
-        assert acc == float(y[r].item()), r
-    del xs
+    threads = len(os.sched_getaffinity(0))
+    blk = 1 << 20
+    for r0 in (0, n // 3 // blk * blk, 2 * n // 3 // blk * blk + 12345, n - blk):
+        r1 = r0 + blk
+        rp, offs, vals = oracle.gen_fill_parallel(n, b, kmax, seed, cdf, table, r0, r1, threads)
+        lo, hi = max(0, r0 - b), min(n, r1 + b)
+        xw = oracle.gen_normal(21, lo, hi, table)
+        ref = oracle.spmv_kernel("da", rp, offs, vals, xw, np.empty(blk), 1.0, 0.0,
+                                 x_offset=r0 - lo)
+        got = y[r0:r1].cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), r0
+
+
+def test_power_iteration_50_c5_shaped(cuda):
+    """50 normalised power iterations on a C5-shaped band (n = 2^22, b =
+    32767, Poisson(8)) with the default kernel: every norm and the final
+    iterate bit-exact against the oracle's power iteration."""
+    import os
+    n, b, lam, kmax, seed = 1 << 22, 32767, 8.0, 32, 2027
+    arr = banded_arrays(n, b, lam, kmax, seed, cuda, kinds=("da",))
+    dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"])
+    x0 = normal_vector(n, 11, cuda)
+    x, norms = power_iteration(dm, x0, iters=50, variant="naive")
+    threads = len(os.sched_getaffinity(0))
+    rp, offs, vals = oracle.gen_fill_parallel(n, b, kmax, seed, poisson_cdf(lam, kmax),
+                                              normal_table(), threads=threads)
+    xr = x0.cpu().numpy()
+    s = np.sqrt(oracle.fold_ordered(oracle.sumsq_chunks(xr, 1 << 16)))
+    for k in range(50):
+        xr = oracle.spmv("da", rp, offs, vals, xr, alpha=1.0 / s, threads=threads)
+        s = np.sqrt(oracle.fold_ordered(oracle.sumsq_chunks(xr, 1 << 16)))
+        assert s == norms[k], k
+    assert np.array_equal(x.cpu().numpy().view(np.uint64), (xr * (1.0 / s)).view(np.uint64))
 
 
 def test_nnz_above_2_31_int64_rowptr(cuda):
@@ -109,7 +136,7 @@ def test_nnz_above_2_31_int64_rowptr(cuda):
     rng = np.random.default_rng(2)
     rows = np.concatenate([[0, n - 1, n // 2], rng.integers(n - (1 << 20), n, 40),
                            rng.integers(0, n, 40)])
-    for kernel in ("wstream", "rowblock", "sliced"):
+    for kernel in ("tiled", "rowblock", "sliced"):
         y = torch.empty(n, dtype=torch.float64, device=cuda)
         dm.spmv_into(x, y, 1.0, 0.0, kernel, 0)
         for r in rows.tolist():

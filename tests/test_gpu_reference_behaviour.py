@@ -152,3 +152,29 @@ def test_narrow_index_widths(cuda):
     x = np.array([1.0, 2.0, 3.0, 4.0])
     want = dense_matvec(dense_of(a), x)
     assert np.array_equal(dg.spmv(a, x), want) and np.array_equal(dg.spmv(d, x), want)
+
+
+def test_host_arrays_on_a_caller_stream(cuda):
+    """Host x / y with a non-default stream: the copies and the kernel are
+    ordered on that stream, pinned and pageable y alike; the
+    stream is kept busy first so a missing dependency would show."""
+    import torch
+    from paper_2307_06305_b200.workloads import laplacian_2d, uniform_x
+    a = dg.to_dacsr(laplacian_2d(300), 16)
+    x = uniform_x(a.ncols, 4)
+    y0 = np.random.default_rng(5).uniform(-1, 1, a.nrows)
+    want = oracle.spmv("da", a.rowptr, a.colids, a.values, x, y0.copy(), 0.5, 2.0)
+    s = torch.cuda.Stream()
+    busy = torch.ones(1 << 24, device=cuda)
+    for pinned in (False, True):
+        with torch.cuda.stream(s):
+            for _ in range(20):
+                busy.mul_(1.0000001)  # a backlog on the stream before the call
+        if pinned:
+            y = torch.from_numpy(y0.copy()).pin_memory().numpy()
+        else:
+            y = y0.copy()
+        out = dg.spmv(a, x, y, 0.5, 2.0, stream=s)
+        assert out is y
+        s.synchronize()
+        assert np.array_equal(y, want), pinned
