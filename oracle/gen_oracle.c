@@ -5,7 +5,7 @@
  * The reference has no such generator (its generate.py builds small
  * triplet matrices, /root/reference/pkg/src/dacsr/generate.py:37-64); the
  * product generates C3/C5 on the device (paper_2307_06305_b200/csrc/
- * gen_kernels.cu) and this file is the independent checker that the device
+ * gen.cu) and this file is the independent checker that the device
  * output is the documented matrix.  Every row is a pure function of
  * (seed, row), so tests verify sampled rows of a 2^28-row device matrix
  * without materialising it on the host.
