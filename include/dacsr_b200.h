@@ -151,12 +151,12 @@ typedef struct {
  * = the entries of row j of lane l whose column falls in the tile (0..15).
  * The group's entries start at ent_ptr[g], tile after tile.  Inside a tile,
  * lane l's entries (its rows j = 0..15 in order, each row's entries in
- * column order) form a list L_l, stored in pair steps: entries 2q and 2q+1
- * of L_l sit at tile_base + 2 * (sum_{q' < q} |{l' : |L_l'| > 2q'}| +
- * |{l' < l : |L_l'| > 2q}|) and the slot after it (a list of odd length
- * ends in one zero slot), so the lanes of a warp read pair step q of their
- * lists as one packed run of 2-entry vectors.  Every tile segment has an
- * even length.  Entries are bit-for-bit copies; every row's entries keep
+ * column order) form a list L_l, stored in steps of G = step_group
+ * entries: entries Gq .. Gq+G-1 of L_l sit at tile_base + G * (sum_{q' < q}
+ * |{l' : |L_l'| > Gq'}| + |{l' < l : |L_l'| > Gq}|) (a list whose length
+ * is not a multiple of G ends in zero slots), so the lanes of a warp read
+ * step q of their lists as one packed run of G-entry vectors.  Every tile
+ * segment is a multiple of G long.  Entries are bit-for-bit copies; every row's entries keep
  * their order, so a lane folding its list in order reproduces the naive
  * sum.
  * Rows with more than 15 entries inside one tile are left out (counts 0,
@@ -170,8 +170,8 @@ typedef struct {
   int64_t col0;             /* first column of tile 0 (= cmin)              */
   int64_t cmax;             /* last column any entry uses                   */
   int32_t tile_cols;        /* columns per tile (x tile = tile_cols values) */
-  int32_t reserved;
-  int64_t total;            /* slots in the layout (entries + pair padding) */
+  int32_t step_group;       /* entries per lane per packed step: 2 or 4     */
+  int64_t total;            /* slots in the layout (entries + padding)      */
   int64_t nblocks;          /* cnt_ptr[ngroups]                             */
   const int64_t* ent_ptr;   /* ngroups + 1                                  */
   const int64_t* cnt_ptr;   /* ngroups + 1                                  */
@@ -301,6 +301,8 @@ int dacsr_tiles_count(const dacsr_matrix_t* a, const dacsr_tiles_t* t, int32_t* 
                       int32_t* ent_counts_dev, int32_t* ovf_counts_dev, void* stream);
 int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int64_t* ovf_ptr_dev,
                      void* stream);
+/* The step_group the TILED kernel of this build reads (layouts must match). */
+int32_t dacsr_tiles_step_group(void);
 
 /* Variant the library would run for DACSR_VARIANT_AUTO. */
 int32_t dacsr_select_variant(const dacsr_stats_t* stats, int32_t order);

@@ -91,7 +91,7 @@ class Tiles(ctypes.Structure):
     """dacsr_tiles_t: the band-tiled device layout (512-row groups x column tiles)."""
     _fields_ = [("row_start", ctypes.c_int64), ("row_end", ctypes.c_int64),
                 ("ngroups", ctypes.c_int64), ("col0", ctypes.c_int64), ("cmax", ctypes.c_int64),
-                ("tile_cols", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("tile_cols", ctypes.c_int32), ("step_group", ctypes.c_int32),
                 ("total", ctypes.c_int64), ("nblocks", ctypes.c_int64),
                 ("ent_ptr", ctypes.c_void_p), ("cnt_ptr", ctypes.c_void_p),
                 ("tile_lo", ctypes.c_void_p), ("counts", ctypes.c_void_p),
@@ -127,6 +127,7 @@ _SIGNATURES = {
     "dacsr_tiles_extent": ([_P(Matrix), _i64, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_tiles_count": ([_P(Matrix), _P(Tiles), _vp, _vp, _vp, _vp], ctypes.c_int),
     "dacsr_tiles_fill": ([_P(Matrix), _P(Tiles), _vp, _vp], ctypes.c_int),
+    "dacsr_tiles_step_group": ([], _i32),
     "dacsr_plan_chunks": ([_P(Matrix), _i64, _i64, _i32, _i32, _vp, _vp, _P(Plan), _vp],
                           ctypes.c_int),
     "dacsr_spmv": ([_P(Matrix), _P(Plan), _i32, _i32, _vp, _i64, _vp, _d, _d, _i64, _i64, _vp],

@@ -56,6 +56,8 @@ const char* dacsr_version(void) { return "dacsr_b200 0.1.0 (sm_100a)"; }
 
 const char* dacsr_last_error(void) { return g_last_error; }
 
+int32_t dacsr_tiles_step_group(void) { return DACSR_TILED_G; }
+
 // Selection by row statistics (measured per config):
 //  * scattered gathers (random wide bands, C3/C5): TILED, x staged in smem;
 //  * everything else with enough rows (stencils, RCM orders, skew: C1, C2,

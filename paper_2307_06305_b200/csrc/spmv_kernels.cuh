@@ -1375,6 +1375,7 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       if (!p || !p->tiles) return DACSR_ERR_PLAN;
       const dacsr_tiles_t* td = p->tiles;
       if (q.rs < td->row_start || q.re > td->row_end || td->tile_cols < 64 ||
+          td->step_group != DACSR_TILED_G ||
           td->tile_cols > 65536 || (td->tile_cols & 15) ||
           td->ngroups != (td->row_end - td->row_start + 511) / 512 ||
           (td->ngroups > 0 && (!td->ent_ptr || !td->cnt_ptr || !td->tile_lo || !td->skip)) ||

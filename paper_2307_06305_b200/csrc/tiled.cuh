@@ -28,6 +28,9 @@
 // thread at 96 registers (measured: spills) instead of 128
 constexpr int kTileWarps = 15;  // consumer warps (groups) per CTA
 constexpr int kTileRows = 16;   // rows per lane
+#ifndef DACSR_TILED_G
+#define DACSR_TILED_G 2  // entries per lane per packed step (layout step_group)
+#endif
 #ifndef DACSR_TILED_XBUFS
 #define DACSR_TILED_XBUFS 2
 #endif
@@ -163,6 +166,40 @@ __device__ __forceinline__ void pair_ld_cs(const int64_t* p, bool pred, int64_t&
   a = x;
   b = y;
 }
+// four consecutive elements (p aligned to 4 * sizeof(T))
+template <class T, class R>
+__device__ __forceinline__ void quad_ld_cs(const T* p, bool pred, R* o) {
+  if constexpr (sizeof(T) >= 4) {  // two pair loads
+    pair_ld_cs(p, pred, o[0], o[1]);
+    pair_ld_cs(p + 2, pred, o[2], o[3]);
+  } else if constexpr (sizeof(T) == 2) {  // 8 bytes: 4 x 16 bit
+    uint32_t w0, w1;
+    asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.b32 {%0, %1}, [%2];\n\t}"
+                 : "=r"(w0), "=r"(w1) : "l"(p), "r"(static_cast<unsigned>(pred)));
+    if constexpr (std::is_same<T, int16_t>::value) {
+      o[0] = static_cast<int>(static_cast<int16_t>(w0 & 0xffffu));
+      o[1] = static_cast<int>(w0) >> 16;
+      o[2] = static_cast<int>(static_cast<int16_t>(w1 & 0xffffu));
+      o[3] = static_cast<int>(w1) >> 16;
+    } else if constexpr (std::is_same<T, __half>::value) {
+      o[0] = __ushort_as_half(static_cast<unsigned short>(w0 & 0xffffu));
+      o[1] = __ushort_as_half(static_cast<unsigned short>(w0 >> 16));
+      o[2] = __ushort_as_half(static_cast<unsigned short>(w1 & 0xffffu));
+      o[3] = __ushort_as_half(static_cast<unsigned short>(w1 >> 16));
+    } else {
+      o[0] = __ushort_as_bfloat16(static_cast<unsigned short>(w0 & 0xffffu));
+      o[1] = __ushort_as_bfloat16(static_cast<unsigned short>(w0 >> 16));
+      o[2] = __ushort_as_bfloat16(static_cast<unsigned short>(w1 & 0xffffu));
+      o[3] = __ushort_as_bfloat16(static_cast<unsigned short>(w1 >> 16));
+    }
+  } else {  // int8: 4 bytes
+    const uint32_t w = pair_ld_cs_b32(p, pred);
+    o[0] = static_cast<int>(static_cast<int8_t>(w & 0xffu));
+    o[1] = static_cast<int>(static_cast<int8_t>((w >> 8) & 0xffu));
+    o[2] = static_cast<int>(static_cast<int8_t>((w >> 16) & 0xffu));
+    o[3] = static_cast<int>(static_cast<int8_t>(w >> 24));
+  }
+}
 #undef DACSR_PAIR_PRED
 
 // acc += p (round to nearest) when pred, as one predicated DADD
@@ -212,6 +249,8 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
                  int64_t g_last, int64_t rs, int64_t re, int xbuf) {
   using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
   constexpr int U = DACSR_TILED_BATCH;
+  constexpr int G = DACSR_TILED_G;
+  static_assert(U % G == 0, "batch must be whole step groups");
   extern __shared__ __align__(128) unsigned char dsm[];
   VT* const xs = reinterpret_cast<VT*>(dsm);
   const size_t xstride = tiled_xbuf_bytes<VT>(xbuf) / sizeof(VT);
@@ -325,7 +364,7 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
   // the operator segment of a tile: its lanes' lists rounded up to pairs
   auto seg_slots = [&](uint64_t w) {
     return static_cast<int>(
-        __reduce_add_sync(0xffffffffu, static_cast<unsigned>((nibble_sum(w) + 1) & ~1)));
+        __reduce_add_sync(0xffffffffu, static_cast<unsigned>((nibble_sum(w) + G - 1) / G * G)));
   };
   uint64_t ncn0 = 0, ncn1 = 0;
   auto load_first_counts = [&](const ChunkMeta& q2) {
@@ -400,20 +439,25 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         asm("" : "+l"(vt));
         asm("" : "+l"(ct));
         uint32_t lp = 0;
-        // batch of U steps = U/2 pair steps: positions from the pair-step
-        // ballots, then every operator load of the batch issued (2-entry
+        // batch of U steps = U/G packed steps: positions from the step
+        // ballots, then every operator load of the batch issued (G-entry
         // vector loads, predicated asm, program order)
-        constexpr int UP = U / 2;
+        constexpr int UP = U / G;
         auto load_batch = [&](int q0, OT* off, VT* val) {
 #pragma unroll
           for (int u = 0; u < UP; ++u) {
-            const bool act = 2 * (q0 + u) < total;
+            const bool act = G * (q0 + u) < total;
             const unsigned msk = __ballot_sync(0xffffffffu, act);
-            const uint32_t o = lp + 2 * __popc(msk & below);
-            lp += 2 * __popc(msk);
-            DACSR_CHECK(!act || pos + o + 1 < ta.total);
-            pair_ld_cs(elem_addr_u32(ct, o), act, off[2 * u], off[2 * u + 1]);
-            pair_ld_cs(elem_addr_u32(vt, o), act, val[2 * u], val[2 * u + 1]);
+            const uint32_t o = lp + G * __popc(msk & below);
+            lp += G * __popc(msk);
+            DACSR_CHECK(!act || pos + o + G - 1 < ta.total);
+            if constexpr (G == 2) {
+              pair_ld_cs(elem_addr_u32(ct, o), act, off[2 * u], off[2 * u + 1]);
+              pair_ld_cs(elem_addr_u32(vt, o), act, val[2 * u], val[2 * u + 1]);
+            } else {
+              quad_ld_cs(elem_addr_u32(ct, o), act, off + 4 * u);
+              quad_ld_cs(elem_addr_u32(vt, o), act, val + 4 * u);
+            }
           }
         };
         auto fold_batch = [&](int k0, const OT* off, const VT* val) {
@@ -473,11 +517,11 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         int k0 = 0;
         if (kmax > 0) load_batch(0, offA, valA);
         while (k0 < kmax) {
-          if (k0 + U < kmax) load_batch((k0 + U) / 2, offB, valB);
+          if (k0 + U < kmax) load_batch((k0 + U) / G, offB, valB);
           fold_batch(k0, offA, valA);
           k0 += U;
           if (k0 >= kmax) break;
-          if (k0 + U < kmax) load_batch((k0 + U) / 2, offA, valA);
+          if (k0 + U < kmax) load_batch((k0 + U) / G, offA, valA);
           fold_batch(k0, offB, valB);
           k0 += U;
         }

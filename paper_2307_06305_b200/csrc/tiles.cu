@@ -70,7 +70,7 @@ __global__ void extent_kernel(const RP* __restrict__ rp, const CI* __restrict__ 
 
 struct TileGeom {
   int64_t rs, re, col0;
-  int T;
+  int T, G;
   __device__ __forceinline__ int64_t tile(int64_t c) const { return (c - col0) / T; }
 };
 
@@ -140,7 +140,7 @@ __global__ void tiles_count_kernel(const RP* __restrict__ rp, const CI* __restri
             ++total;
           }
         }
-        slots += (total + 1) & ~1;
+        slots += (total + geo.G - 1) / geo.G * geo.G;
       }
     }
     for (int o = 16; o > 0; o >>= 1) slots += __shfl_xor_sync(0xffffffffu, slots, o);
@@ -218,24 +218,23 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
         }
         return cur[j] + used++;
       };
-      for (int s = 0; s < kmax; s += 2) {  // pair step: list entries s, s + 1
+      for (int s = 0; s < kmax; s += geo.G) {  // step group: list entries s .. s + G - 1
         const bool act = s < total;
         const unsigned m = __ballot_sync(0xffffffffu, act);
         if (act) {
-          const int64_t dst = pos + 2 * __popc(m & below);
-          const int64_t a = next_src();
-          t_inner[dst] = raw_ci[a];
-          t_values[dst] = v[a];
-          if (s + 1 < total) {
-            const int64_t b2 = next_src();
-            t_inner[dst + 1] = raw_ci[b2];
-            t_values[dst + 1] = v[b2];
-          } else {
-            t_inner[dst + 1] = IT(0);
-            t_values[dst + 1] = VB(0);
+          const int64_t dst = pos + geo.G * __popc(m & below);
+          for (int e = 0; e < geo.G; ++e) {
+            if (s + e < total) {
+              const int64_t a = next_src();
+              t_inner[dst + e] = raw_ci[a];
+              t_values[dst + e] = v[a];
+            } else {
+              t_inner[dst + e] = IT(0);
+              t_values[dst + e] = VB(0);
+            }
           }
         }
-        pos += 2 * __popc(m);
+        pos += geo.G * __popc(m);
       }
 #pragma unroll
       for (int jj = 0; jj < kRowsPerLane; ++jj) cur[jj] += n[jj];
@@ -302,6 +301,7 @@ bool geometry_ok(const dacsr_matrix_t* a, const dacsr_tiles_t* t) {
   return a && t && a->rowptr && t->row_start >= 0 && t->row_end >= t->row_start &&
          t->row_end <= a->nrows && t->ngroups == (t->row_end - t->row_start + 511) / 512 &&
          t->tile_cols >= 64 && t->tile_cols <= 65536 && (t->tile_cols & 15) == 0 &&
+         (t->step_group == 2 || t->step_group == 4) &&
          (a->nnz == 0 || (a->colids && a->values));
 }
 
@@ -339,7 +339,7 @@ int dacsr_tiles_count(const dacsr_matrix_t* a, const dacsr_tiles_t* t, int32_t* 
     return DACSR_ERR_ARG;
   if (t->ngroups == 0) return DACSR_OK;
   auto st = static_cast<cudaStream_t>(stream);
-  const TileGeom geo{t->row_start, t->row_end, t->col0, t->tile_cols};
+  const TileGeom geo{t->row_start, t->row_end, t->col0, t->tile_cols, t->step_group};
   const int g = grid_for_groups(t->ngroups, 8);
   return by_matrix_types(a, [&](auto kc, auto rp0, auto ci0, auto) {
     constexpr int KIND = decltype(kc)::value;
@@ -362,7 +362,7 @@ int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int6
     return DACSR_ERR_ARG;
   if (t->ngroups == 0) return DACSR_OK;
   auto st = static_cast<cudaStream_t>(stream);
-  const TileGeom geo{t->row_start, t->row_end, t->col0, t->tile_cols};
+  const TileGeom geo{t->row_start, t->row_end, t->col0, t->tile_cols, t->step_group};
   const int g = grid_for_groups(t->ngroups, 4);
   return by_matrix_types(a, [&](auto kc, auto rp0, auto ci0, auto vb0) {
     constexpr int KIND = decltype(kc)::value;

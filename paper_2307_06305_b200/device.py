@@ -359,7 +359,8 @@ class DeviceMatrix:
                 cmin = cmax = 0
             tile_lo = torch.zeros(max(ng, 1), dtype=torch.int32, device=dev)
             skip = torch.zeros(max(32 * ng, 1), dtype=torch.int16, device=dev)  # uint16 bits
-            tl = _native.Tiles(rs, re, ng, cmin, cmax, tile_cols, 0, 0, 0, None, None,
+            tl = _native.Tiles(rs, re, ng, cmin, cmax, tile_cols, L.dacsr_tiles_step_group(), 0, 0,
+                               None, None,
                                tile_lo.data_ptr(), None, skip.data_ptr(), None, None, 0, None)
             cnt = torch.zeros(3, max(ng, 1), dtype=torch.int32, device=dev)
             _native.check(L.dacsr_tiles_count(ctypes.byref(self.desc), ctypes.byref(tl),
@@ -397,7 +398,8 @@ class DeviceMatrix:
             return None
         _, tl, tensors = self._tiled
         ng = max(1, tl.ngroups)
-        return {"tile_cols": tl.tile_cols, "col0": tl.col0, "cmax": tl.cmax,
+        return {"tile_cols": tl.tile_cols, "step_group": tl.step_group, "col0": tl.col0,
+                "cmax": tl.cmax,
                 "groups": tl.ngroups, "tile_blocks": tl.nblocks,
                 "tiles_per_group": tl.nblocks / ng, "entries": tl.total, "n_ovf": tl.n_ovf,
                 "count_bytes_per_row": 8 * tl.nblocks * 32 / max(1, tl.row_end - tl.row_start),

@@ -41,11 +41,12 @@ def untile(dm):
             n = [[(int(nib[l]) >> (4 * j)) & 15 for j in range(16)] for l in range(32)]
             tot = [sum(v) for v in n]
             lists = [[] for _ in range(32)]
-            for q in range((max(tot) + 1) // 2):
+            G = tl.step_group
+            for q in range((max(tot) + G - 1) // G):
                 for l in range(32):
-                    if 2 * q < tot[l]:
-                        lists[l] += [pos, pos + 1]
-                        pos += 2
+                    if G * q < tot[l]:
+                        lists[l] += list(range(pos, pos + G))
+                        pos += G
             for l in range(32):
                 slots = iter(lists[l])
                 for j in range(16):
