@@ -316,6 +316,16 @@ int dacsr_spmv(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t varian
                int32_t order, const void* x, int64_t x_offset, void* y, double alpha,
                double beta, int64_t row_start, int64_t row_end, void* stream);
 
+/* dacsr_spmv with alpha read from DEVICE memory by the kernel (at the
+ * epilogue, after the previous grid on the stream completed): iterative
+ * methods whose alpha comes from a device reduction (the power iteration's
+ * 1 / ||y||) run without host round trips and can be graph-captured.  There
+ * is no alpha == 0 short-cut here (the kernel always runs). */
+int dacsr_spmv_dev_alpha(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t variant,
+                         int32_t order, const void* x, int64_t x_offset, void* y,
+                         const double* alpha_dev, double beta, int64_t row_start, int64_t row_end,
+                         void* stream);
+
 /* spmv with HOST x / y, copies overlapped with the kernels: rows split into
  * the row ranges of plans[0..npieces) (ascending, covering the rows); piece
  * p needs x[0, min(ncols, row_end_p + w)) with w the bandwidth (max |col -
@@ -341,6 +351,14 @@ int dacsr_sumsq_chunks(const void* y, int32_t values_dtype, int64_t n, int64_t c
                        double* partial, void* stream);
 /* out[0] = sum of partial[0..m) in index order (one thread, exact order). */
 int dacsr_sum_ordered(const double* partial, int64_t m, double* out, void* stream);
+/* Power-iteration norm on the device: s = sqrt(sum of partial[0..m) in index
+ * order), *norm_out = s (if norm_out), *alpha_out = 1 / s (IEEE sqrt and
+ * division, round to nearest: Python's math.sqrt and 1.0 / s). */
+int dacsr_norm_alpha(const double* partial, int64_t m, double* norm_out, double* alpha_out,
+                     void* stream);
+/* y = (T)(*beta_dev * (double)y) for f64 / f32 y, beta read from device memory. */
+int dacsr_scale_dev(void* y, int32_t values_dtype, int64_t n, const double* beta_dev,
+                    void* stream);
 
 /* Reference-named kernel entry points (one per _numba_kernels.py function;
  * int32 rowptr, DA int16 offsets / CSR int32 colids, the paper's layout).

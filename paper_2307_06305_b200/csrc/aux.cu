@@ -153,6 +153,26 @@ __global__ void sum_ordered_kernel(const double* p, int64_t m, double* out) {
   *out = t;
 }
 
+// the power iteration's norm on the device: s = sqrt(ordered fold of the
+// chunk partials), norms[k] = s, alpha = 1 / s — the same correctly rounded
+// operations as Python's math.sqrt and 1.0 / s
+__global__ void norm_alpha_kernel(const double* p, int64_t m, double* norm_out,
+                                  double* alpha_out) {
+  double t = 0.0;
+  for (int64_t i = 0; i < m; ++i) t = __dadd_rn(t, p[i]);
+  const double sq = __dsqrt_rn(t);
+  if (norm_out) *norm_out = sq;
+  *alpha_out = __ddiv_rn(1.0, sq);
+}
+
+template <class VT>
+__global__ void scale_dev_kernel(VT* y, int64_t n, const double* beta) {
+  const double b = *beta;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    store_rounded(y + i, __dmul_rn(b, to_f64(y[i])));
+}
+
 // warp per row
 template <int KIND, class RP, class CI>
 __global__ void bandwidth_kernel(const void* rpv, const CI* ci, int64_t nrows,
@@ -356,6 +376,27 @@ int dacsr_sumsq_chunks(const void* y, int32_t vdt, int64_t n, int64_t chunk, dou
   else if (vdt == DACSR_F32) sumsq_kernel<float><<<static_cast<unsigned>(m), 256, 0, st>>>(static_cast<const float*>(y), n, chunk, partial);
   else return DACSR_ERR_DTYPE;
   return check_launch("sumsq_kernel");
+}
+
+int dacsr_norm_alpha(const double* partial, int64_t m, double* norm_out, double* alpha_out,
+                     void* stream) {
+  if (!partial || m < 0 || !alpha_out) return DACSR_ERR_ARG;
+  norm_alpha_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(partial, m, norm_out,
+                                                                     alpha_out);
+  return check_launch("norm_alpha_kernel");
+}
+
+int dacsr_scale_dev(void* y, int32_t vdt, int64_t n, const double* beta_dev, void* stream) {
+  if (!y || !beta_dev || n < 0) return DACSR_ERR_ARG;
+  if (n == 0) return DACSR_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const int g = grid_for(n, 256);
+  switch (vdt) {
+    case DACSR_F64: scale_dev_kernel<double><<<g, 256, 0, st>>>(static_cast<double*>(y), n, beta_dev); break;
+    case DACSR_F32: scale_dev_kernel<float><<<g, 256, 0, st>>>(static_cast<float*>(y), n, beta_dev); break;
+    default: return DACSR_ERR_DTYPE;
+  }
+  return check_launch("scale_dev_kernel");
 }
 
 int dacsr_sum_ordered(const double* partial, int64_t m, double* out, void* stream) {

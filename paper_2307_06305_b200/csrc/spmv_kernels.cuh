@@ -54,6 +54,10 @@ struct Scal {
   double alpha, beta;
   int order;
   int64_t long_len;
+  // alpha read from device memory at the epilogue (power iteration: the
+  // previous norm's 1/s, computed on the device); nullptr: `alpha`
+  const double* alpha_dev = nullptr;
+  __device__ __forceinline__ double a() const { return alpha_dev ? __ldg(alpha_dev) : alpha; }
 };
 
 struct Chunks {
@@ -105,7 +109,7 @@ __device__ void long_row(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int64_t 
     double part = 0.0;
     for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) part = __dadd_rn(part, get(i));
     const double t = block_sum_tree(part, scratch);
-    if (threadIdx.x == 0) epilogue(m.y, r, t, s.alpha, s.beta);
+    if (threadIdx.x == 0) epilogue(m.y, r, t, s.a(), s.beta);
     __syncthreads();
     return;
   }
@@ -134,7 +138,7 @@ __device__ void long_row(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int64_t 
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) epilogue(m.y, r, acc.result(), s.alpha, s.beta);
+  if (threadIdx.x == 0) epilogue(m.y, r, acc.result(), s.a(), s.beta);
   __syncthreads();
 }
 
@@ -151,7 +155,7 @@ __device__ void process_rows(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int6
       continue;
     }
     StagedGet<KIND, RP, CI, VT> get{m, sv, si, lo, hi, r};
-    epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
+    epilogue(m.y, r, row_sum(s.order, b, e, get), s.a(), s.beta);
   }
   __syncthreads();
   const int nl = *n_long;
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(256)
        r < row_end; r += stride) {
     const int64_t b = ldg(m.rp + r), e = ldg(m.rp + r + 1);
     auto get = [&](int64_t i) { return m.prod_global(r, i); };
-    epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
+    epilogue(m.y, r, row_sum(s.order, b, e, get), s.a(), s.beta);
   }
 }
 
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(256)
     for (int64_t i = b + sub; i < e; i += G) acc = __dadd_rn(acc, m.prod_global(r, i));
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-    if (sub == 0 && r < row_end) epilogue(m.y, r, acc, s.alpha, s.beta);
+    if (sub == 0 && r < row_end) epilogue(m.y, r, acc, s.a(), s.beta);
   }
 }
 
@@ -346,7 +350,7 @@ __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s
     double part = 0.0;
     for (int64_t i = b + lane; i < e; i += 32) part = __dadd_rn(part, get(i));
     for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-    if (lane == 0) epilogue(m.y, r, part, s.alpha, s.beta);
+    if (lane == 0) epilogue(m.y, r, part, s.a(), s.beta);
     return;
   }
   constexpr int kPer = 4;  // products per lane per batch
@@ -374,7 +378,7 @@ __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s
     }
   }
   __syncwarp();
-  if (lane == 0) epilogue(m.y, r, acc.result(), s.alpha, s.beta);
+  if (lane == 0) epilogue(m.y, r, acc.result(), s.a(), s.beta);
 }
 
 // Chunks the planner listed as not fitting the staging window: one warp per
@@ -399,7 +403,7 @@ __device__ __noinline__ void complex_chunks(const Mat<KIND, RP, CI, VT> m, Scal 
     const bool is_long = (e - b) > s.long_len;
     if (r < re && !is_long) {
       auto get = [&](int64_t i) { return m.prod_global(r, i); };
-      epilogue(m.y, r, row_sum(s.order, b, e, get), s.alpha, s.beta);
+      epilogue(m.y, r, row_sum(s.order, b, e, get), s.a(), s.beta);
     }
     unsigned longs = __ballot_sync(0xffffffffu, r < re && is_long);
     while (longs) {
@@ -650,7 +654,7 @@ __global__ void __launch_bounds__(256, DACSR_WSTREAM_MINB)
 #endif
           const VT* xr = KIND == DACSR_KIND_DA ? xbase + r : xbase;
           epilogue(m.y, r, staged_dot<ORDER>(sv + kk, si + kk, static_cast<int>(e - b), xr),
-                   s.alpha, s.beta);
+                   s.a(), s.beta);
         }
       }
     }
@@ -849,7 +853,7 @@ __device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, co
     const double acc = slice_row_dot<B, OT>(m, r, width, n, xr,
                                             [&](int j) { return ldcs(pi + 32 * j); },
                                             [&](int j) { return ldcs(pv + 32 * j); });
-    if (n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+    if (n >= 0) epilogue(m.y, r, acc, s.a(), s.beta);
   }
 }
 
@@ -1001,7 +1005,7 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
                                    [&](int j) { return ldcs(pi + 32 * j); },
                                    [&](int j) { return ldcs(pv + 32 * j); }, B, acc);
       }
-      if (cur.n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+      if (cur.n >= 0) epilogue(m.y, r, acc, s.a(), s.beta);
       const Meta nxt2 = derive(raw2);
       stage(nxt2);
       cur = nxt;
@@ -1033,7 +1037,7 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
       acc = slice_row_dot<B, OT>(m, r, cur.width, cur.n, xr,
                                  [&](int j) { return ldg(pi + 32 * j); },
                                  [&](int j) { return ldg(pv + 32 * j); });
-    if (cur.n >= 0) epilogue(m.y, r, acc, s.alpha, s.beta);
+    if (cur.n >= 0) epilogue(m.y, r, acc, s.a(), s.beta);
     const Meta nxt2 = derive(raw2);
     stage(nxt2);
     cur = nxt;
@@ -1074,6 +1078,7 @@ struct Req {
   double alpha, beta;
   int64_t rs, re;
   cudaStream_t stream;
+  const double* alpha_dev = nullptr;
 };
 
 // per-value-type launchers (one translation unit each)
@@ -1189,7 +1194,7 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
   if (rows <= 0) return DACSR_OK;
   const int order = q.order;
   const bool exact = order != DACSR_ORDER_TREE;
-  Scal s{q.alpha, q.beta, order, 0};
+  Scal s{q.alpha, q.beta, order, 0, q.alpha_dev};
   const int sms = sm_count();
   const bool can_bulk = aligned16(a->values) && aligned16(a->colids);
 

@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
       for (int j = 0; j < kTileRows; ++j) {
         const int64_t r = lrow + 32 * j;
         if (r >= rs && r < re && !((sk >> j) & 1u))
-          epilogue(m.y, r, lds_f64(wa + 256u * j), s.alpha, s.beta);
+          epilogue(m.y, r, lds_f64(wa + 256u * j), s.a(), s.beta);
       }
     }
     __syncwarp();

@@ -92,6 +92,7 @@ class DeviceMatrix:
         self._tiled = None   # (plan, Tiles, tensors) once build_tiles ran
         self._launch_cache = {}
         self._spmv_fn = _native.lib().dacsr_spmv
+        self._spmv_dev_alpha_fn = _native.lib().dacsr_spmv_dev_alpha
         self.tuned_kernel = None
         if plan:
             self.build_plan(cap=cap, long_len=long_len)
@@ -568,6 +569,8 @@ class DeviceMatrix:
                   row_start=None, row_end=None, stream=None):
         """Launch y = alpha*A@x + beta*y on device tensors (no validation
         beyond the C ABI's; ``spmv`` is the validating entry point).
+        ``alpha`` may be a one-element float64 CUDA tensor: the kernel reads it
+        from device memory (dacsr_spmv_dev_alpha; no alpha == 0 short-cut).
 
         The (variant, order, row range) -> (code, plan) resolution is cached
         per matrix, so a launch costs one ctypes call (a few microseconds of
@@ -587,9 +590,14 @@ class DeviceMatrix:
             sp = torch.cuda.current_stream(self.device).cuda_stream
         else:
             sp = stream.cuda_stream
-        status = self._spmv_fn(desc, plan_ref, code, order_code,
-                               x.data_ptr() if x is not None else None, x_offset,
-                               y.data_ptr(), alpha, beta, rs, re, sp)
+        if isinstance(alpha, torch.Tensor):  # alpha in device memory (one float64)
+            status = self._spmv_dev_alpha_fn(desc, plan_ref, code, order_code,
+                                             x.data_ptr() if x is not None else None, x_offset,
+                                             y.data_ptr(), alpha.data_ptr(), beta, rs, re, sp)
+        else:
+            status = self._spmv_fn(desc, plan_ref, code, order_code,
+                                   x.data_ptr() if x is not None else None, x_offset,
+                                   y.data_ptr(), alpha, beta, rs, re, sp)
         if status:
             _native.check(status, "dacsr_spmv")
         return y

@@ -202,6 +202,8 @@ class CudaLocalOp:
             dm.spmv_into(x_ext, y, alpha, 0.0, self.kernels[which], self.order,
                          x_offset=self.x_offset, row_start=r0, row_end=r1, stream=stream)
 
+    device_norm = True  # the norm and the next alpha stay on the device
+
     def partials(self, y):
         from .power import chunk_partials
         return chunk_partials(y, self.chunk).clone()
@@ -209,6 +211,14 @@ class CudaLocalOp:
     def fold(self, allp):
         from .power import fold_ordered
         return float(fold_ordered(allp).item())
+
+    def norm_alpha(self, allp, norm_out, alpha_out):
+        from .power import norm_alpha
+        norm_alpha(allp, norm_out, alpha_out)
+
+    def scale(self, x, factor):
+        from .power import scale_by_device_factor
+        scale_by_device_factor(x, factor)
 
 
 def dist_spmv(op, x_ext, y, alpha, plan, group=None, overlap=True):
@@ -251,6 +261,21 @@ def power_iteration(op, plan, x0_own, iters, group=None, overlap=True, counts=No
     bufs = [torch.zeros(plan.length, dtype=x0_own.dtype, device=dev) for _ in range(2)]
     own = plan.own_slice()
     bufs[0][own] = x0_own
+    if getattr(op, "device_norm", False) and counts is not None:
+        # no host round trip: alpha and the norms live on the device
+        alpha = torch.empty(1, dtype=torch.float64, device=dev)
+        norms = torch.empty(iters + 1, dtype=torch.float64, device=dev)
+        op.norm_alpha(gather_partials(op.partials(x0_own), group, counts), norms[0:1], alpha)
+        cur = 0
+        for k in range(iters):
+            nxt = 1 - cur
+            dist_spmv(op, bufs[cur], bufs[nxt][own], alpha, plan, group, overlap)
+            op.norm_alpha(gather_partials(op.partials(bufs[nxt][own]), group, counts),
+                          norms[k + 1:k + 2], alpha)
+            cur = nxt
+        x = bufs[cur][own].clone()
+        op.scale(x, alpha)
+        return x, norms[1:].tolist()
     s_prev = math.sqrt(op.fold(gather_partials(op.partials(x0_own), group, counts)))
     norms = []
     cur = 0

@@ -49,33 +49,102 @@ def chunked_sumsq(y, chunk=DEFAULT_CHUNK, stream=None):
     return float(out.item())
 
 
+def norm_alpha(partials, norm_out, alpha_out, stream=None):
+    """On the device: s = sqrt(ordered fold of partials), norm_out[0] = s,
+    alpha_out[0] = 1 / s (Python's math.sqrt and 1.0 / s, bit for bit)."""
+    _native.check(_native.lib().dacsr_norm_alpha(
+        ctypes.c_void_p(partials.data_ptr()), partials.numel(),
+        ctypes.c_void_p(norm_out.data_ptr()) if norm_out is not None else None,
+        ctypes.c_void_p(alpha_out.data_ptr()), _stream_ptr(stream)), "dacsr_norm_alpha")
+
+
+def scale_by_device_factor(x, factor, stream=None):
+    """x *= factor[0] (factor a float64 device scalar), one rounding."""
+    _native.check(_native.lib().dacsr_scale_dev(
+        ctypes.c_void_p(x.data_ptr()), _native.dtype_code(x.dtype), x.numel(),
+        ctypes.c_void_p(factor.data_ptr()), _stream_ptr(stream)), "dacsr_scale_dev")
+
+
+class PowerIteration:
+    """``iters`` normalised power steps on one GPU, entirely on the device:
+    each step is the SpMV with alpha read from device memory
+    (dacsr_spmv_dev_alpha), the chunked sum of squares of the result and the
+    norm / next alpha (dacsr_norm_alpha) — no host round trip, so the whole
+    run can be captured once in a CUDA graph and replayed.
+
+    Semantics (identical to the host loop it replaced): x_0 = x0 / ||x0||;
+    y_k = alpha_k * A y_{k-1} with alpha_k = 1/s_{k-1} (alpha_0 = 1/||x0||,
+    y_{-1} = x0); s_k = ||y_k||; the result is y / s.
+    """
+
+    def __init__(self, dm, x0, iters=50, chunk=DEFAULT_CHUNK, variant="naive", order=0,
+                 graph=False):
+        from .spmv import _EXACT, kernel_for, resolve_variant
+        if variant in _EXACT or variant == "auto":
+            name, order = resolve_variant(variant)
+            variant = kernel_for(dm, name, order)
+        self.dm, self.iters, self.chunk, self.variant, self.order = dm, iters, chunk, variant, order
+        self.x0 = x0
+        self.bufs = [torch.empty_like(x0), torch.empty_like(x0)]
+        dev = x0.device
+        m = (x0.numel() + chunk - 1) // chunk
+        self.partials = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+        self.alpha = torch.empty(1, dtype=torch.float64, device=dev)
+        self.norms = torch.empty(iters + 1, dtype=torch.float64, device=dev)
+        self.graph = None
+        if graph:
+            self._launch()  # warm: derived layout, launch-config caches
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            with torch.cuda.graph(g, stream=s):
+                self._launch()
+            torch.cuda.synchronize()
+            self.graph = g
+
+    def _launch(self, stream=None):
+        dm, chunk = self.dm, self.chunk
+        self.bufs[0].copy_(self.x0)
+        chunk_partials(self.bufs[0], chunk, stream, out=self.partials)
+        norm_alpha(self.partials, self.norms[0:1], self.alpha, stream)
+        cur = 0
+        for k in range(self.iters):
+            dm.spmv_into(self.bufs[cur], self.bufs[1 - cur], self.alpha, 0.0, self.variant,
+                         self.order, stream=stream)
+            cur = 1 - cur
+            chunk_partials(self.bufs[cur], chunk, stream, out=self.partials)
+            norm_alpha(self.partials, self.norms[k + 1:k + 2], self.alpha, stream)
+        self.cur = cur
+
+    def run(self):
+        """Enqueue the whole run (graph replay when captured); returns x."""
+        if self.graph is not None:
+            self.graph.replay()
+            self.cur = self.iters % 2
+        else:
+            self._launch()
+        return self.bufs[self.cur]
+
+    def result(self):
+        """(x_iters, norms) after run(): x = y / s (a copy), norms on the host."""
+        x = self.bufs[self.cur].clone()
+        scale_by_device_factor(x, self.alpha)
+        return x, self.norms[1:].tolist()
+
+
 def power_iteration(dm, x0, iters=50, chunk=DEFAULT_CHUNK, variant="naive", order=0,
                     stream=None):
-    """Run ``iters`` normalised power steps from x0 (device tensor).
+    """Run ``iters`` normalised power steps from x0 (device tensor); returns
+    (x, norms) with norms[k] = ||A x_k|| (see PowerIteration)."""
+    with torch.cuda.stream(stream) if stream is not None else _nullctx():
+        pi = PowerIteration(dm, x0, iters, chunk, variant, order)
+        pi.run()
+        return pi.result()
 
-    ``variant``: a kernel name, or a reference variant name ("naive", ...)
-    resolved by the library's selection for this matrix.
 
-    Returns (x, norms) with norms[k] = ||A x_k|| and x = x_iters.
-    x_0 = x0 / ||x0||; y_k = alpha_k * A y_{k-1} with alpha_k = 1/s_{k-1}
-    (alpha_0 = 1/||x0||, y_{-1} = x0); s_k = ||y_k||; x_iters = y/s.
-    """
-    from .spmv import _EXACT, kernel_for, resolve_variant
-    if variant in _EXACT or variant == "auto":
-        name, order = resolve_variant(variant)
-        variant = kernel_for(dm, name, order)
-    bufs = [x0.clone(), torch.empty_like(x0)]
-    s_prev = math.sqrt(chunked_sumsq(x0, chunk, stream))
-    norms = []
-    cur = 0
-    for _ in range(iters):
-        alpha = 1.0 / s_prev
-        dm.spmv_into(bufs[cur], bufs[1 - cur], alpha, 0.0, variant, order, stream=stream)
-        cur = 1 - cur
-        s_prev = math.sqrt(chunked_sumsq(bufs[cur], chunk, stream))
-        norms.append(s_prev)
-    x = bufs[cur]
-    _native.check(_native.lib().dacsr_scale(
-        ctypes.c_void_p(x.data_ptr()), _native.dtype_code(x.dtype), x.numel(), 1.0 / s_prev,
-        _stream_ptr(stream)), "dacsr_scale")
-    return x, norms
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False

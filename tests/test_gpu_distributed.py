@@ -147,3 +147,32 @@ def test_nnz_above_2_31_int64_rowptr(cuda):
                 acc = acc + oracle.gen_value(b, seed, r, o, table) * xv
             assert acc == float(y[r].item()), (kernel, r)
         del y
+
+
+@pytest.mark.parametrize("kernel", ["tiled", "sliced_pipe", "wstream", "scalar", "rowblock"])
+def test_device_alpha_matches_host_alpha(cuda, kernel):
+    """dacsr_spmv_dev_alpha reads alpha from device memory: the same bits as
+    passing it by value (the power iteration's 1/s never leaves the GPU)."""
+    arr = banded_arrays(N, B, LAM, KMAX, SEED, cuda)
+    dm = DeviceMatrix("da", N, N, arr["rowptr"], arr["offsets"], arr["values"])
+    x = normal_vector(N, 9, cuda)
+    a = 1.0 / 3.7
+    y1 = torch.empty(N, dtype=torch.float64, device=cuda)
+    y2 = torch.full((N,), 2.0, dtype=torch.float64, device=cuda)
+    dm.spmv_into(x, y1, a, 0.0, kernel, 0)
+    dm.spmv_into(x, y2, torch.tensor([a], dtype=torch.float64, device=cuda), 0.0, kernel, 0)
+    assert torch.equal(y1.view(torch.int64), y2.view(torch.int64))
+
+
+def test_power_iteration_graph_replay_matches_eager(cuda):
+    from paper_2307_06305_b200.power import PowerIteration
+    arr = banded_arrays(N, B, LAM, KMAX, SEED, cuda)
+    dm = DeviceMatrix("da", N, N, arr["rowptr"], arr["offsets"], arr["values"])
+    x0 = normal_vector(N, 11, cuda)
+    x_e, n_e = power_iteration(dm, x0, iters=8, chunk=4096)
+    pi = PowerIteration(dm, x0, iters=8, chunk=4096, graph=True)
+    for _ in range(2):  # replays are repeatable
+        pi.run()
+        x_g, n_g = pi.result()
+        assert n_g == n_e
+        assert torch.equal(x_g.view(torch.int64), x_e.view(torch.int64))
