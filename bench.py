@@ -390,18 +390,17 @@ def suite_builders():
     return {"c1": c1, "c2": c2, "c2f32": c2f32, "c2bf16": c2bf16, "c4": c4, "c5slab": c5slab}
 
 
-def run_c5(args, world, rank, local):
+def measure_c5(steps, warmup, local=0):
     """Config C5 on one GPU: 50 normalised power iterations x <- A x / ||A x||
-    on the 2^28-row band, DA-CSR i16, generated on the device.  One step =
-    the 50 iterations."""
+    on the 2^28-row band, DA-CSR i16, generated on the device, the 50
+    iterations (SpMV with alpha read on the device, chunked norm, next alpha)
+    captured once in a CUDA graph.  Returns (per-step seconds, record)."""
     import torch
     from paper_2307_06305_b200.device import DeviceMatrix
     from paper_2307_06305_b200.gen import banded_arrays, normal_vector
-    from paper_2307_06305_b200.harness import ClockSampler
     from paper_2307_06305_b200.power import PowerIteration
     from paper_2307_06305_b200.spmv import kernel_for
     from paper_2307_06305_b200.workloads import BANDED_CONFIGS
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n, b, lam, kmax, seed = BANDED_CONFIGS["c5"]
     t0 = time.time()
@@ -412,40 +411,52 @@ def run_c5(args, world, rank, local):
     traffic = traffic_of(n, dm.nnz, dm.oindex_width // 8, 2, 8)
     iters = 50
     kname = kernel_for(dm, "exact", 0)
-    # the 50 iterations (SpMV with alpha read on the device, chunked norm,
-    # next alpha) captured once in a CUDA graph: no host round trip
     pi = PowerIteration(dm, x0, iters=iters, variant=kname, graph=True)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         pi.run()
     torch.cuda.synchronize()
     times = []
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            pi.run()
-            e1.record()
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1) / 1e3)
+    for _ in range(steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pi.run()
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
     _, norms = pi.result()
     step = sum(times) / len(times)
+    rec = {"workload": "C5: power iteration, 50 iters, banded n=2^28 b=32767 "
+                       "clip(Poisson(8),1,32), DA-CSR i16",
+           "value": round(iters * traffic / step / 1e9, 1), "unit": "GB/s",
+           "ms_per_step": round(step * 1e3, 3), "steps": steps,
+           "nnz": dm.nnz, "rowptr": str(dm.rowptr.dtype), "bytes_per_spmv": traffic,
+           "build_s": round(build_s, 1), "final_norm": norms[-1], "kernel": kname,
+           "cuda_graph": True}
+    del pi, dm, arr
+    torch.cuda.empty_cache()
+    return times, rec
+
+
+def run_c5(args, world, rank, local):
+    """The C5 line at one GPU (``--workload c5``)."""
+    import torch
+    from paper_2307_06305_b200.harness import ClockSampler
+    torch.cuda.set_device(local)
+    with ClockSampler(local) as clocks:
+        times, rec = measure_c5(args.steps, args.warmup, local)
     peak, peak_src = peaks()
     line = {
-        "metric": METRIC, "value": round(iters * traffic / step / 1e9, 1), "unit": "GB/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(step * 1e3, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C5: power iteration, 50 iters, banded n=2^28 b=32767 "
-                               "clip(Poisson(8),1,32), DA-CSR i16",
-                   "nnz": dm.nnz, "rowptr": str(dm.rowptr.dtype), "bytes_per_spmv": traffic,
-                   "build_s": round(build_s, 1), "final_norm": norms[-1], "kernel": kname,
-                   "cuda_graph": True},
-        "roofline": {"bound": "hbm", "achieved": round(iters * traffic / step / 1e9, 1),
-                     "peak": peak, "unit": "GB/s",
-                     "frac": round(iters * traffic / step / 1e9 / peak, 4), "traffic": None,
+        "metric": METRIC, "value": rec["value"], "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {k: v for k, v in rec.items() if k not in ("value", "unit", "ms_per_step",
+                                                            "steps")},
+        "roofline": {"bound": "hbm", "achieved": rec["value"], "peak": peak, "unit": "GB/s",
+                     "frac": round(rec["value"] / peak, 4), "traffic": None,
                      "peak_source": peak_src},
-        "gpu_launches": args.steps * (iters * 3 + 3),
+        "gpu_launches": args.steps * (50 * 3 + 3),
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -574,10 +585,16 @@ def run_ours(args):
                            f"spmv(DacsrMatrix, x, y, 1, 0, ParallelRowBlock({threads}, "
                            f"'{numba_t[1]}')) on C3 rows [0, 2^22), reference time_kernel"}
                 if numba_t else {"unavailable": why})}
+    del dm, dmc, mats
+    torch.cuda.empty_cache()
     if not args.no_suite:
+        # config C5 at one GPU: the base of the N>1 strong-scaling runs
+        # (bench.py --gpus N runs the same 50 iterations over N ranks)
+        try:
+            _, line["c5_power_iteration_1gpu"] = measure_c5(3, 1, local)
+        except Exception as exc:
+            line["c5_power_iteration_1gpu"] = {"error": f"{type(exc).__name__}: {exc}"}
         suite = {}
-        del dm, dmc, mats
-        torch.cuda.empty_cache()
         builders = suite_builders()
         for name in args.suite.split(","):
             if name in builders:
