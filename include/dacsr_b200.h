@@ -292,9 +292,9 @@ int dacsr_slices_medium_fill(const dacsr_matrix_t* a, const dacsr_slices_t* s, v
  *    ovf_counts[g] = rows left out; t->tile_lo and t->skip filled.
  * 3. dacsr_tiles_fill (every t field set; ovf_ptr = scanned ovf_counts):
  *    counts, inner, values, ovf_rows.
- * 64 <= tile_cols <= 65536, a multiple of 16; the TILED kernel keeps three x
- * tiles in shared memory, so it needs tile_cols * sizeof(value) <= 54 KiB
- * (DACSR_ERR_PLAN otherwise; DeviceMatrix uses 48 KiB). */
+ * 64 <= tile_cols <= 65536, a multiple of 16; the TILED kernel keeps its x
+ * tiles in shared memory, so tile_cols <= dacsr_tiles_max_cols(values dtype)
+ * (DACSR_ERR_PLAN otherwise). */
 int dacsr_tiles_extent(const dacsr_matrix_t* a, int64_t row_start, int64_t row_end,
                        int64_t* out2_dev, void* stream);
 int dacsr_tiles_count(const dacsr_matrix_t* a, const dacsr_tiles_t* t, int32_t* nt_counts_dev,
@@ -303,6 +303,10 @@ int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int6
                      void* stream);
 /* The step_group the TILED kernel of this build reads (layouts must match). */
 int32_t dacsr_tiles_step_group(void);
+/* Widest tile_cols whose x ring fits the TILED kernel's shared memory for
+ * this value type (DeviceMatrix.build_tiles' default: fewer, larger tiles
+ * cost less per entry). */
+int32_t dacsr_tiles_max_cols(int32_t values_dtype);
 
 /* Variant the library would run for DACSR_VARIANT_AUTO. */
 int32_t dacsr_select_variant(const dacsr_stats_t* stats, int32_t order);

@@ -128,6 +128,7 @@ _SIGNATURES = {
     "dacsr_tiles_count": ([_P(Matrix), _P(Tiles), _vp, _vp, _vp, _vp], ctypes.c_int),
     "dacsr_tiles_fill": ([_P(Matrix), _P(Tiles), _vp, _vp], ctypes.c_int),
     "dacsr_tiles_step_group": ([], _i32),
+    "dacsr_tiles_max_cols": ([_i32], _i32),
     "dacsr_plan_chunks": ([_P(Matrix), _i64, _i64, _i32, _i32, _vp, _vp, _P(Plan), _vp],
                           ctypes.c_int),
     "dacsr_spmv": ([_P(Matrix), _P(Plan), _i32, _i32, _vp, _i64, _vp, _d, _d, _i64, _i64, _vp],

@@ -58,6 +58,20 @@ const char* dacsr_last_error(void) { return g_last_error; }
 
 int32_t dacsr_tiles_step_group(void) { return DACSR_TILED_G; }
 
+int32_t dacsr_tiles_max_cols(int32_t values_dtype) {
+  static const int kB[8] = {1, 2, 4, 8, 4, 8, 2, 2};
+  if (values_dtype < DACSR_F32 || values_dtype > DACSR_BF16) return 0;
+  const size_t vb = kB[values_dtype];
+  const size_t budget = 227 * 1024;
+  const size_t fixed = size_t(kTileWarps) * (kTileRows + 1) * 32 * 8 + 16 * kTileXBufs;
+  if (budget <= fixed) return 0;
+  // kTileXBufs x ((T + 16 / vb) * vb rounded up to 128 bytes) must fit
+  const size_t per_buf = ((budget - fixed) / kTileXBufs) & ~size_t(127);
+  int64_t t = static_cast<int64_t>(per_buf / vb) - static_cast<int64_t>(16 / vb);
+  t &= ~int64_t(15);
+  return static_cast<int32_t>(std::min<int64_t>(t, 65536));
+}
+
 // Selection by row statistics (measured per config):
 //  * scattered gathers (random wide bands, C3/C5): TILED, x staged in smem;
 //  * everything else with enough rows (stencils, RCM orders, skew: C1, C2,

@@ -331,8 +331,8 @@ class DeviceMatrix:
     def build_tiles(self, tile_cols=None, stream=None):
         """Build the band-tiled device layout (dacsr_tiles_t) of rows
         [row_start, row_end) for the TILED kernel: 512-row groups, columns in
-        tiles of ``tile_cols`` (default 64 KiB of x values, 8192 for f64:
-        the kernel keeps two x tiles in shared memory),
+        tiles of ``tile_cols`` (default: the widest whose x ring fits the
+        kernel's shared memory, dacsr_tiles_max_cols: 10112 for f64),
         each group's entries stored tile by tile in the order its lanes fold
         them.  A bit-for-bit copy of the entries (about the operator's size
         again in HBM, plus half a byte per row and tile of counts).  Returns
@@ -340,12 +340,13 @@ class DeviceMatrix:
         L = _native.lib()
         if self.plan is None:
             self.build_plan(stream=stream)
+        widest = int(L.dacsr_tiles_max_cols(self.desc.values_dtype))
         if tile_cols is None:
-            tile_cols = 65536 // self.values.element_size()
+            tile_cols = widest
         tile_cols = int(tile_cols)
-        if tile_cols < 64 or tile_cols % 16 or tile_cols * self.values.element_size() > 65536:
-            raise ValueError("tile_cols must be a multiple of 16, >= 64, and its x tile at most "
-                             "64 KiB")
+        if tile_cols < 64 or tile_cols % 16 or tile_cols > widest:
+            raise ValueError(f"tile_cols must be a multiple of 16 in [64, {widest}] (the x tiles "
+                             "live in shared memory)")
         rs, re = self.row_start, self.row_end
         dev = self.device
         sp = _stream_ptr(stream)

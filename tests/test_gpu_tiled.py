@@ -136,7 +136,8 @@ def test_narrow_values_match_exact_kernels(cuda, dtype):
     got = dm.spmv_into(x, torch.empty(n, dtype=dtype, device=cuda), 1.0, 0.0, "tiled")
     as_int = {4: torch.int32, 2: torch.int16}[dtype.itemsize]
     assert torch.equal(got.view(as_int), want.view(as_int))
-    assert dm.tiles_info()["tile_cols"] == 65536 // dtype.itemsize
+    from paper_2307_06305_b200 import _native
+    assert dm.tiles_info()["tile_cols"] == _native.lib().dacsr_tiles_max_cols(dm.desc.values_dtype)
 
 
 def test_skewed_rows_and_default_selection(cuda):
