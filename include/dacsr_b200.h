@@ -143,12 +143,15 @@ typedef struct {
  * derived copy of the entries for matrices whose rows spread over a wide
  * band (x gathers would miss L1 one sector per entry).
  *
- * Rows come in groups of 512: lane l (0..31) of group g holds rows
- * row_start + 512g + 32j + l, j = 0..15.  Columns come in tiles of
- * tile_cols: tile t = [col0 + t*tile_cols, col0 + (t+1)*tile_cols).  Group g
- * spans tiles tile_lo[g] .. tile_lo[g] + (cnt_ptr[g+1] - cnt_ptr[g]) - 1; for
- * its k-th tile, counts[(cnt_ptr[g] + k) * 32 + l] holds 16 nibbles, nibble j
- * = the entries of row j of lane l whose column falls in the tile (0..15).
+ * Rows come in groups of 512 (row slot s = 32j + l, j = 0..15, l = 0..31:
+ * row row_start + 512g + s).  Columns come in tiles of tile_cols: tile t =
+ * [col0 + t*tile_cols, col0 + (t+1)*tile_cols).  Group g spans tiles
+ * tile_lo[g] .. tile_lo[g] + (cnt_ptr[g+1] - cnt_ptr[g]) - 1; its k-th tile
+ * is block b = cnt_ptr[g] + k.  In block b lane l folds, for j = 0..15, row
+ * slot 32j + (l ^ m_j), m_j = nibble j of masks[b] (a per-tile lane remap
+ * that evens out the lanes' list lengths); counts[b * 32 + l] holds 16
+ * nibbles, nibble j = the entries of that row whose column falls in the
+ * tile (0..15).
  * The group's entries start at ent_ptr[g], tile after tile.  Inside a tile,
  * lane l's entries (its rows j = 0..15 in order, each row's entries in
  * column order) form a list L_l, stored in steps of G = step_group
@@ -182,6 +185,7 @@ typedef struct {
   const void* values;       /* total + 16, the matrix's values dtype        */
   int64_t n_ovf;
   const int64_t* ovf_rows;  /* n_ovf, ascending                             */
+  const uint64_t* masks;    /* nblocks: lane remap nibbles of each block     */
 } dacsr_tiles_t;
 
 /* dacsr_plan_t.flags: the SLICED kernels skip the L2 bulk prefetch of the

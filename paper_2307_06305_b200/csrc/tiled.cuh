@@ -45,6 +45,7 @@ struct TileArgs {
   const int64_t* __restrict__ cnt_ptr;
   const int32_t* __restrict__ tile_lo;
   const uint64_t* __restrict__ counts;
+  const uint64_t* __restrict__ masks;
   const uint16_t* __restrict__ skip;
   const CI* __restrict__ ci;
   const VT* __restrict__ v;
@@ -343,19 +344,22 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
   // row sums: lane l's row j at wacc + (32 j + l) * 8; row 16 is a dummy
   // slot (the first "switch" of a tile parks the empty running sum there)
   double* const wacc = accs + warp * (kTileRows + 1) * 32;
-  const uint32_t wa = smem_addr(wacc) + 8u * lane;
+  const uint32_t wab = smem_addr(wacc);
+  const uint32_t wa = wab + 8u * lane;
   const uint32_t xs0 = smem_addr(xs);
-  const size_t vpad = ta.total + 16;  // inner / values carry 16 padding entries
+  // segment starts are multiples of G entries (every lane list is padded
+  // to whole step groups) and inner / values carry 16 padding entries, so
+  // rounding a segment out to 16-byte boundaries stays inside the arrays
   auto prefetch_segment = [&](int64_t p0, int n) {
     if (lane != 0 || n <= 0) return;
-    const uintptr_t v0 = reinterpret_cast<uintptr_t>(ta.v + p0) & ~uintptr_t(15);
-    const uintptr_t v1 = min(reinterpret_cast<uintptr_t>(ta.v + p0 + n) + 15,
-                             reinterpret_cast<uintptr_t>(ta.v + vpad)) & ~uintptr_t(15);
-    const uintptr_t i0 = reinterpret_cast<uintptr_t>(ta.ci + p0) & ~uintptr_t(15);
-    const uintptr_t i1 = min(reinterpret_cast<uintptr_t>(ta.ci + p0 + n) + 15,
-                             reinterpret_cast<uintptr_t>(ta.ci + vpad)) & ~uintptr_t(15);
-    if (v1 > v0) prefetch_l2_bulk(reinterpret_cast<const void*>(v0), static_cast<uint32_t>(v1 - v0));
-    if (i1 > i0) prefetch_l2_bulk(reinterpret_cast<const void*>(i0), static_cast<uint32_t>(i1 - i0));
+    const uintptr_t v0 = reinterpret_cast<uintptr_t>(ta.v + p0);
+    const uintptr_t va = v0 & ~uintptr_t(15);
+    prefetch_l2_bulk(reinterpret_cast<const void*>(va),
+                     static_cast<uint32_t>(((v0 + n * sizeof(VT) + 15) & ~uintptr_t(15)) - va));
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(ta.ci + p0);
+    const uintptr_t ia = i0 & ~uintptr_t(15);
+    prefetch_l2_bulk(reinterpret_cast<const void*>(ia),
+                     static_cast<uint32_t>(((i0 + n * sizeof(CI) + 15) & ~uintptr_t(15)) - ia));
   };
   int rb = 0;
   uint32_t rph = 0;
@@ -366,12 +370,15 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
     return static_cast<int>(
         __reduce_add_sync(0xffffffffu, static_cast<unsigned>((nibble_sum(w) + G - 1) / G * G)));
   };
-  uint64_t ncn0 = 0, ncn1 = 0;
+  // count words and lane remap words of a block: (counts, masks)
+  uint64_t ncn0 = 0, ncn1 = 0, nmw0 = 0, nmw1 = 0;
   auto load_first_counts = [&](const ChunkMeta& q2) {
     const int64_t c0 = __shfl_sync(0xffffffffu, q2.cnt0, warp);
     const int64_t c1 = __shfl_sync(0xffffffffu, q2.cnt1, warp);
     ncn0 = c1 > c0 ? ldg(ta.counts + c0 * 32 + lane) : 0;
+    nmw0 = c1 > c0 ? ldg(ta.masks + c0) : 0;
     ncn1 = c1 > c0 + 1 ? ldg(ta.counts + (c0 + 1) * 32 + lane) : 0;
+    nmw1 = c1 > c0 + 1 ? ldg(ta.masks + c0 + 1) : 0;
   };
   load_first_counts(nq);
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
     int64_t pos = __shfl_sync(0xffffffffu, q.ent, warp);
 #pragma unroll
     for (int j = 0; j < kTileRows; ++j) sts_f64(wa + 256u * j, 0.0);
-    uint64_t cn0 = ncn0, cn1 = ncn1;
+    uint64_t cn0 = ncn0, cn1 = ncn1, mw0 = nmw0, mw1 = nmw1;
     // the operator segment of the group's first tile into L2 now, every
     // later one a tile ahead of its fold (bulk prefetch; measured: without
     // it C3 runs 11 % slower, two tiles ahead 4 % slower)
@@ -399,15 +406,26 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
     }
     // rows of lane l: row0 + 512g + 32j + l
     const int64_t lrow = ta.row0 + 512 * g + lane;
+    // byte offset of column 0 relative to x buffer element 0 of tile tlo
+    // (32-bit wrap-around); tile starts advance by T columns and T is a
+    // multiple of 16, so every tile shares tile col0's 16-byte shift
+    uint32_t xoff = static_cast<uint32_t>((ta.col0 - tile_shift(ta.col0) + tlo * ta.T) *
+                                          static_cast<int64_t>(sizeof(VT)));
+    const uint32_t tstep = static_cast<uint32_t>(ta.T * sizeof(VT));
+    const uint32_t grow_b =
+        static_cast<uint32_t>((ta.row0 + 512 * g) * static_cast<int64_t>(sizeof(VT)));
     for (int64_t t = tlo; t <= thi; ++t) {
       const int64_t k = t - gtlo;
       const bool mine = has && k >= 0 && k < gnt;
-      uint64_t cur = 0;
+      uint64_t cur = 0, mw = 0;
       int total = 0;
       if (mine) {
         cur = cn0;
+        mw = mw0;
         cn0 = cn1;
+        mw0 = mw1;
         cn1 = k + 2 < gnt ? ldg(ta.counts + (cbase + k + 2) * 32 + lane) : 0;
+        mw1 = k + 2 < gnt ? ldg(ta.masks + cbase + k + 2) : 0;
         total = nibble_sum(cur);
         if (k + 1 < gnt) {
           const int n = seg_slots(cn0);
@@ -418,19 +436,21 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
       if (t == thi) load_first_counts(nq);  // the next chunk's first count words
       mbar_wait_sleep(&full[rb], rph);
       if (mine) {
-        const int64_t cs = ta.col0 + t * ta.T;
-        const int64_t d = cs - tile_shift(cs);  // column of x buffer element 0
+        DACSR_CHECK(xoff == static_cast<uint32_t>((ta.col0 + t * ta.T - tile_shift(ta.col0 + t * ta.T)) *
+                                                  static_cast<int64_t>(sizeof(VT))));
         const uint32_t xsa = xs0 + static_cast<uint32_t>(rb * xstride * sizeof(VT));
-        // DA: x of entry (row j, offset o) at xr + o * sizeof(VT), xr = &xbuf[row - d];
-        // CSR: at xc + c * sizeof(VT), xc = &xbuf[-d] (32-bit wrap-around arithmetic)
-        const uint32_t xr0 = xsa + static_cast<uint32_t>((lrow - d) * static_cast<int64_t>(sizeof(VT)));
-        const uint32_t xc = xsa - static_cast<uint32_t>(d * static_cast<int64_t>(sizeof(VT)));
+        // d = column of x buffer element 0.  DA: x of entry (row, offset o)
+        // at xr + o * sizeof(VT), xr = &xbuf[row - d]; CSR: at xc + c *
+        // sizeof(VT), xc = &xbuf[-d] (32-bit wrap-around arithmetic).  Row
+        // slot s of the group: xr = xg + s * sizeof(VT), its sum at wab + 8s.
+        const uint32_t xc = xsa - xoff;
+        const uint32_t xg = xc + grow_b;
         const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
         // rows of this tile with entries (bit j), consumed in order
         uint32_t nz = nonzero_nibbles(cur);
         int rem = 0;
         uint32_t acc_a = wa + 32u * 8u * kTileRows;  // dummy slot
-        uint32_t xr = xr0;
+        uint32_t xr = xg;
         double acc = 0.0;
         const VT* vt = ta.v + pos;
         const CI* ct = ta.ci + pos;
@@ -467,25 +487,26 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
             // the sums), branch-free, so every x read of the batch can issue
             // before the first sum of the batch is formed
             uint32_t xrs[U];
-            uint32_t swm = 0, jpk = 0;
+            uint32_t swm = 0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const bool sw = u < left && rem == 0;
-              const int jn = __ffs(nz) - 1;
+              const int jn = (__ffs(nz) - 1) & 15;
               const uint32_t nz2 = nz & (nz - 1);
-              const int rem2 = static_cast<int>((cur >> (4 * (jn & 15))) & 15u);
+              const int rem2 = static_cast<int>((cur >> (4 * jn)) & 15u);
+              const uint32_t slot = (static_cast<uint32_t>(jn) << 5) |
+                                    (lane ^ static_cast<uint32_t>((mw >> (4 * jn)) & 15u));
               nz = sw ? nz2 : nz;
               rem = (sw ? rem2 : rem) - 1;
-              xr = sw ? xr0 + static_cast<uint32_t>(32 * jn * sizeof(VT)) : xr;
+              xr = sw ? xg + slot * static_cast<uint32_t>(sizeof(VT)) : xr;
               swm |= sw ? 1u << u : 0u;
-              jpk |= sw ? static_cast<uint32_t>(jn) << (4 * u) : 0u;
               xrs[u] = xr;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               if ((swm >> u) & 1u) {  // this lane's next row of the tile
                 sts_f64(acc_a, acc);
-                acc_a = wa + 256u * ((jpk >> (4 * u)) & 15u);
+                acc_a = wab + (xrs[u] - xg) * static_cast<uint32_t>(8 / sizeof(VT));
                 acc = lds_f64(acc_a);
               }
               const uint32_t xa = xrs[u] + static_cast<uint32_t>(static_cast<int>(off[u]) * static_cast<int>(sizeof(VT)));
@@ -501,7 +522,8 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
                 const int j = __ffs(nz) - 1;
                 nz &= nz - 1;
                 rem = static_cast<int>((cur >> (4 * j)) & 15u);
-                acc_a = wa + 256u * j;
+                acc_a = wab + 8u * ((static_cast<uint32_t>(j) << 5) |
+                                    (lane ^ static_cast<uint32_t>((mw >> (4 * j)) & 15u)));
                 acc = lds_f64(acc_a);
               }
               const uint32_t xa = xc + static_cast<uint32_t>(off[u] * static_cast<OT>(sizeof(VT)));
@@ -528,6 +550,7 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         sts_f64(acc_a, acc);
         pos += lp;
       }
+      xoff += tstep;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[rb]);
       if (++rb == kTileXBufs) {

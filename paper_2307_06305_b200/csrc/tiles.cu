@@ -8,8 +8,10 @@
 // entries of its rows that fall inside it; the layout built here is the same
 // entries re-laid in exactly that consumption order:
 //
-//   group g (512 rows: lane l holds rows 512g + 32j + l, j = 0..15)
-//     tile t (tile_lo[g] ..):  counts[32]  — lane l: 16 nibbles (entries of
+//   group g (512 rows, row slot 32j + l)
+//     tile t (tile_lo[g] ..):  mask        — 16 nibbles m_j: lane l folds
+//                                           row slot 32j + (l ^ m_j)
+//                              counts[32]  — lane l: 16 nibbles (entries of
 //                                           its row j inside the tile)
 //                              entries     — lane lists L_l stored in pair
 //                                           steps (pair step q: entries 2q,
@@ -23,7 +25,13 @@
 // in the reference's naive order (_numba_kernels.py:82-91).  Entries are
 // copied as raw bits.
 //
-// Passes (warp per group): extent (min / max column), count, fill.
+// The lane remap evens out the lanes' list lengths: with a fixed row ->
+// lane map a tile's lists are Poisson-ragged (C3: the longest list of a
+// warp is ~1.4x the mean, and every lane of the warp steps through it); the
+// masks, chosen greedily row slot by row slot, bring that near 1.1x.
+//
+// Passes (warp per group): extent (min / max column), count, fill.  Count
+// and fill derive the masks from the same counts with the same function.
 
 #include <algorithm>
 #include <climits>
@@ -66,6 +74,39 @@ __global__ void extent_kernel(const RP* __restrict__ rp, const CI* __restrict__ 
     atomicMin(out, lo);
     atomicMax(out + 1, hi);
   }
+}
+
+// Lane remap of one tile: c[j] = entries of row slot 32j + lane in the
+// tile.  For j = 0..15 in turn, m_j (0..15) minimises (longest list in
+// steps of G, sum of squared list lengths) over the lists so far plus row
+// slots 32j + (l ^ m_j); ties go to the smallest m_j.  Returns the mask
+// word (the same in every lane) and this lane's list length.
+__device__ __forceinline__ uint64_t balance_lanes(const int (&c)[kRowsPerLane], int G, int& total) {
+  const int lane = threadIdx.x & 31;
+  uint64_t mw = 0;
+  int tot = 0;
+#pragma unroll
+  for (int j = 0; j < kRowsPerLane; ++j) {
+    unsigned long long best = ~0ull;
+    int bm = 0;
+    if (__any_sync(0xffffffffu, c[j] != 0)) {
+#pragma unroll 1
+      for (int m = 0; m < 16; ++m) {
+        const int t2 = tot + __shfl_sync(0xffffffffu, c[j], lane ^ m);
+        const unsigned mx = __reduce_max_sync(0xffffffffu, static_cast<unsigned>((t2 + G - 1) / G));
+        const unsigned sq = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(t2 * t2));
+        const unsigned long long key = (static_cast<unsigned long long>(mx) << 32) | sq;
+        if (key < best) {
+          best = key;
+          bm = m;
+        }
+      }
+    }
+    tot += __shfl_sync(0xffffffffu, c[j], lane ^ bm);
+    mw |= static_cast<uint64_t>(bm) << (4 * j);
+  }
+  total = tot;
+  return mw;
 }
 
 struct TileGeom {
@@ -131,15 +172,18 @@ __global__ void tiles_count_kernel(const RP* __restrict__ rp, const CI* __restri
         }
       }
       for (int64_t t = tmin; t <= tmax; ++t) {
-        int total = 0;
+        int c[kRowsPerLane];
 #pragma unroll
         for (int j = 0; j < kRowsPerLane; ++j) {
           const int64_t r = geo.rs + kGroupRows * g + 32 * j + lane;
+          c[j] = 0;
           while (cur[j] < end[j] && geo.tile(entry_col<KIND>(r, ci[cur[j]])) == t) {
             ++cur[j];
-            ++total;
+            ++c[j];
           }
         }
+        int total;
+        balance_lanes(c, geo.G, total);
         slots += (total + geo.G - 1) / geo.G * geo.G;
       }
     }
@@ -163,8 +207,8 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
     TileGeom geo, int64_t ngroups, const int64_t* __restrict__ ent_ptr,
     const int64_t* __restrict__ cnt_ptr, const int32_t* __restrict__ tile_lo,
     const uint16_t* __restrict__ skip, const int64_t* __restrict__ ovf_ptr,
-    uint64_t* __restrict__ counts, IT* __restrict__ t_inner, VB* __restrict__ t_values,
-    int64_t* __restrict__ ovf_rows) {
+    uint64_t* __restrict__ counts, uint64_t* __restrict__ masks, IT* __restrict__ t_inner,
+    VB* __restrict__ t_values, int64_t* __restrict__ ovf_rows) {
   const int lane = threadIdx.x & 31;
   const unsigned below = (1u << lane) - 1u;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -195,9 +239,7 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
     int64_t pos = ent_ptr[g];
     for (int64_t k = 0; k < nt; ++k) {
       const int64_t t = t0 + k;
-      // this tile's entries of each row: [cur[j], cur[j] + n[j])
-      uint64_t nib = 0;
-      int total = 0;
+      // this tile's entries of each own row: [cur[j], cur[j] + n[j])
       int n[kRowsPerLane];
 #pragma unroll
       for (int j = 0; j < kRowsPerLane; ++j) {
@@ -205,18 +247,30 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
         int c = 0;
         while (cur[j] + c < end[j] && geo.tile(entry_col<KIND>(r, ci[cur[j] + c])) == t) ++c;
         n[j] = c;
-        total += c;
-        nib |= static_cast<uint64_t>(c) << (4 * j);
+      }
+      int total;
+      const uint64_t mw = balance_lanes(n, geo.G, total);
+      // the rows this lane folds: slot 32j + (lane ^ m_j)
+      int64_t src[kRowsPerLane];
+      int nr[kRowsPerLane];
+      uint64_t nib = 0;
+#pragma unroll
+      for (int j = 0; j < kRowsPerLane; ++j) {
+        const int from = lane ^ static_cast<int>((mw >> (4 * j)) & 15u);
+        nr[j] = __shfl_sync(0xffffffffu, n[j], from);
+        src[j] = __shfl_sync(0xffffffffu, cur[j], from);
+        nib |= static_cast<uint64_t>(nr[j]) << (4 * j);
       }
       counts[(cnt_ptr[g] + k) * 32 + lane] = nib;
+      if (lane == 0) masks[cnt_ptr[g] + k] = mw;
       const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
       int j = 0, used = 0;
       auto next_src = [&]() {  // this lane's next list entry
-        while (used == n[j]) {
+        while (used == nr[j]) {
           ++j;
           used = 0;
         }
-        return cur[j] + used++;
+        return src[j] + used++;
       };
       for (int s = 0; s < kmax; s += geo.G) {  // step group: list entries s .. s + G - 1
         const bool act = s < total;
@@ -357,8 +411,8 @@ int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int6
                      void* stream) {
   if (!geometry_ok(a, t) || !ovf_ptr ||
       (t->ngroups > 0 && (!t->ent_ptr || !t->cnt_ptr || !t->tile_lo || !t->skip)) ||
-      (t->nblocks > 0 && !t->counts) || (t->total > 0 && (!t->inner || !t->values)) ||
-      (t->n_ovf > 0 && !t->ovf_rows))
+      (t->nblocks > 0 && (!t->counts || !t->masks)) ||
+      (t->total > 0 && (!t->inner || !t->values)) || (t->n_ovf > 0 && !t->ovf_rows))
     return DACSR_ERR_ARG;
   if (t->ngroups == 0) return DACSR_OK;
   auto st = static_cast<cudaStream_t>(stream);
@@ -373,7 +427,7 @@ int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int6
     tiles_fill_kernel<KIND, RP, CI, IT, VB><<<g, 128, 0, st>>>(
         static_cast<const RP*>(a->rowptr), static_cast<const CI*>(a->colids),
         static_cast<const VB*>(a->values), geo, t->ngroups, t->ent_ptr, t->cnt_ptr, t->tile_lo,
-        t->skip, ovf_ptr, const_cast<uint64_t*>(t->counts),
+        t->skip, ovf_ptr, const_cast<uint64_t*>(t->counts), const_cast<uint64_t*>(t->masks),
         static_cast<IT*>(const_cast<void*>(t->inner)), static_cast<VB*>(const_cast<void*>(t->values)),
         const_cast<int64_t*>(t->ovf_rows));
     return check_launch("tiles_fill_kernel");

@@ -332,7 +332,7 @@ class DeviceMatrix:
         """Build the band-tiled device layout (dacsr_tiles_t) of rows
         [row_start, row_end) for the TILED kernel: 512-row groups, columns in
         tiles of ``tile_cols`` (default: the widest whose x ring fits the
-        kernel's shared memory, dacsr_tiles_max_cols: 10112 for f64),
+        kernel's shared memory, dacsr_tiles_max_cols: 10416 for f64),
         each group's entries stored tile by tile in the order its lanes fold
         them.  A bit-for-bit copy of the entries (about the operator's size
         again in HBM, plus half a byte per row and tile of counts).  Returns
@@ -363,7 +363,8 @@ class DeviceMatrix:
             skip = torch.zeros(max(32 * ng, 1), dtype=torch.int16, device=dev)  # uint16 bits
             tl = _native.Tiles(rs, re, ng, cmin, cmax, tile_cols, L.dacsr_tiles_step_group(), 0, 0,
                                None, None,
-                               tile_lo.data_ptr(), None, skip.data_ptr(), None, None, 0, None)
+                               tile_lo.data_ptr(), None, skip.data_ptr(), None, None, 0, None,
+                               None)
             cnt = torch.zeros(3, max(ng, 1), dtype=torch.int32, device=dev)
             _native.check(L.dacsr_tiles_count(ctypes.byref(self.desc), ctypes.byref(tl),
                                                vp(cnt[0]), vp(cnt[1]), vp(cnt[2]), sp),
@@ -374,13 +375,14 @@ class DeviceMatrix:
                     self._scan(cnt[k, :ng], ptrs[k, :ng + 1], sp)
             nblocks, total, n_ovf = (int(v) for v in ptrs[:, ng].tolist())
             counts = torch.empty(max(32 * nblocks, 1), dtype=torch.int64, device=dev)  # uint64 bits
+            masks = torch.empty(max(nblocks, 1), dtype=torch.int64, device=dev)  # uint64 bits
             inner = torch.zeros(total + 16, dtype=self.colids.dtype, device=dev)
             values = torch.zeros(total + 16, dtype=self.values.dtype, device=dev)
             ovf_rows = torch.empty(max(n_ovf, 1), dtype=torch.int64, device=dev)
             tl.total, tl.nblocks, tl.n_ovf = total, nblocks, n_ovf
             tl.cnt_ptr, tl.ent_ptr = ptrs[0].data_ptr(), ptrs[1].data_ptr()
             tl.counts, tl.inner, tl.values = counts.data_ptr(), inner.data_ptr(), values.data_ptr()
-            tl.ovf_rows = ovf_rows.data_ptr()
+            tl.ovf_rows, tl.masks = ovf_rows.data_ptr(), masks.data_ptr()
             _native.check(L.dacsr_tiles_fill(ctypes.byref(self.desc), ctypes.byref(tl),
                                               vp(ptrs[2]), sp), "dacsr_tiles_fill")
             _sync(stream)
@@ -389,7 +391,7 @@ class DeviceMatrix:
         plan.slices = self._sliced[0].slices if self._sliced is not None else None
         plan.tiles = ctypes.addressof(tl)
         tensors = {"ptrs": ptrs, "tile_lo": tile_lo, "skip": skip, "counts": counts,
-                   "inner": inner, "values": values, "ovf_rows": ovf_rows}
+                   "masks": masks, "inner": inner, "values": values, "ovf_rows": ovf_rows}
         self._tiled = (plan, tl, tensors)
         self._invalidate_launches()
         return plan

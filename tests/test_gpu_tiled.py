@@ -32,6 +32,7 @@ def untile(dm):
     cnt_ptr, ent_ptr = ptrs[0], ptrs[1]
     tile_lo = t["tile_lo"].cpu().numpy()
     counts = t["counts"].cpu().numpy().view(np.uint64)
+    masks = t["masks"].cpu().numpy().view(np.uint64)
     inner, vals = t["inner"].cpu().numpy(), t["values"].cpu().numpy()
     rows = {}
     for g in range(tl.ngroups):
@@ -39,6 +40,7 @@ def untile(dm):
         for k in range(int(cnt_ptr[g + 1] - cnt_ptr[g])):
             nib = counts[(cnt_ptr[g] + k) * 32:(cnt_ptr[g] + k + 1) * 32]
             n = [[(int(nib[l]) >> (4 * j)) & 15 for j in range(16)] for l in range(32)]
+            mw = int(masks[cnt_ptr[g] + k])
             tot = [sum(v) for v in n]
             lists = [[] for _ in range(32)]
             G = tl.step_group
@@ -50,7 +52,7 @@ def untile(dm):
             for l in range(32):
                 slots = iter(lists[l])
                 for j in range(16):
-                    r = tl.row_start + 512 * g + 32 * j + l
+                    r = tl.row_start + 512 * g + 32 * j + (l ^ ((mw >> (4 * j)) & 15))
                     for _ in range(n[l][j]):
                         p = next(slots)
                         rows.setdefault(r, []).append((int(tile_lo[g]) + k, inner[p], vals[p]))
