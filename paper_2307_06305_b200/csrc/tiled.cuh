@@ -114,94 +114,83 @@ __device__ __forceinline__ const T* elem_addr_u32(const T* base, uint32_t o) {
   return p;
 }
 
-// Predicated evict-first load of two consecutive elements (one vector load;
-// p aligned to 2 * sizeof(T)); asm volatile, so a batch's loads are issued
-// in program order before the batch folds.  Outputs are undefined when
-// !pred (every use is predicated or selected away).
+// Predicated evict-first load of a packed step's two consecutive elements
+// (one vector load; p aligned to 2 * sizeof(T)), kept as loaded: two
+// registers for 4- and 8-byte types, one 32-bit word for narrower ones.
+// The loads are asm volatile, so a batch's loads issue in program order
+// before the previous batch folds; narrow elements are unpacked in the fold
+// by pair_elem, also volatile (unpacked at load time, nvcc placed the
+// sign-extensions right behind the loads and every warp sat out the full
+// load latency there).  Words are undefined when !pred (every use is
+// predicated or selected away).
+template <class T>
+struct PairReg {
+  static constexpr bool kPacked = sizeof(T) <= 2;
+  using W = typename std::conditional<kPacked, uint32_t, T>::type;
+  static constexpr int kWords = kPacked ? 1 : 2;
+};
 #define DACSR_PAIR_PRED "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q "
-__device__ __forceinline__ void pair_ld_cs(const double* p, bool pred, double& a, double& b) {
+#define DACSR_ONE_PRED "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q "
+__device__ __forceinline__ void pair_ld_cs(const double* p, bool pred, double* w) {
   asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.f64 {%0, %1}, [%2];\n\t}"
-               : "=d"(a), "=d"(b) : "l"(p), "r"(static_cast<unsigned>(pred)));
+               : "=d"(w[0]), "=d"(w[1]) : "l"(p), "r"(static_cast<unsigned>(pred)));
 }
-__device__ __forceinline__ void pair_ld_cs(const float* p, bool pred, float& a, float& b) {
+__device__ __forceinline__ void pair_ld_cs(const float* p, bool pred, float* w) {
   asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.f32 {%0, %1}, [%2];\n\t}"
-               : "=f"(a), "=f"(b) : "l"(p), "r"(static_cast<unsigned>(pred)));
+               : "=f"(w[0]), "=f"(w[1]) : "l"(p), "r"(static_cast<unsigned>(pred)));
 }
-__device__ __forceinline__ uint32_t pair_ld_cs_b32(const void* p, bool pred) {
-  uint32_t w;
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cs.b32 %0, [%1];\n\t}"
-               : "=r"(w) : "l"(p), "r"(static_cast<unsigned>(pred)));
-  return w;
-}
-__device__ __forceinline__ void pair_ld_cs(const __half* p, bool pred, __half& a, __half& b) {
-  const uint32_t w = pair_ld_cs_b32(p, pred);
-  a = __ushort_as_half(static_cast<unsigned short>(w & 0xffffu));
-  b = __ushort_as_half(static_cast<unsigned short>(w >> 16));
-}
-__device__ __forceinline__ void pair_ld_cs(const __nv_bfloat16* p, bool pred, __nv_bfloat16& a,
-                                           __nv_bfloat16& b) {
-  const uint32_t w = pair_ld_cs_b32(p, pred);
-  a = __ushort_as_bfloat16(static_cast<unsigned short>(w & 0xffffu));
-  b = __ushort_as_bfloat16(static_cast<unsigned short>(w >> 16));
-}
-__device__ __forceinline__ void pair_ld_cs(const int16_t* p, bool pred, int& a, int& b) {
-  const uint32_t w = pair_ld_cs_b32(p, pred);
-  a = static_cast<int>(static_cast<int16_t>(w & 0xffffu));
-  b = static_cast<int>(w) >> 16;
-}
-__device__ __forceinline__ void pair_ld_cs(const int8_t* p, bool pred, int& a, int& b) {
-  unsigned short w;
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cs.b16 %0, [%1];\n\t}"
-               : "=h"(w) : "l"(p), "r"(static_cast<unsigned>(pred)));
-  a = static_cast<int>(static_cast<int8_t>(w & 0xffu));
-  b = static_cast<int>(static_cast<int8_t>(w >> 8));
-}
-__device__ __forceinline__ void pair_ld_cs(const int32_t* p, bool pred, int& a, int& b) {
+__device__ __forceinline__ void pair_ld_cs(const int32_t* p, bool pred, int32_t* w) {
   asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.s32 {%0, %1}, [%2];\n\t}"
-               : "=r"(a), "=r"(b) : "l"(p), "r"(static_cast<unsigned>(pred)));
+               : "=r"(w[0]), "=r"(w[1]) : "l"(p), "r"(static_cast<unsigned>(pred)));
 }
-__device__ __forceinline__ void pair_ld_cs(const int64_t* p, bool pred, int64_t& a, int64_t& b) {
+__device__ __forceinline__ void pair_ld_cs(const int64_t* p, bool pred, int64_t* w) {
   long long x, y;
   asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.s64 {%0, %1}, [%2];\n\t}"
                : "=l"(x), "=l"(y) : "l"(p), "r"(static_cast<unsigned>(pred)));
-  a = x;
-  b = y;
+  w[0] = x;
+  w[1] = y;
 }
-// four consecutive elements (p aligned to 4 * sizeof(T))
-template <class T, class R>
-__device__ __forceinline__ void quad_ld_cs(const T* p, bool pred, R* o) {
-  if constexpr (sizeof(T) >= 4) {  // two pair loads
-    pair_ld_cs(p, pred, o[0], o[1]);
-    pair_ld_cs(p + 2, pred, o[2], o[3]);
-  } else if constexpr (sizeof(T) == 2) {  // 8 bytes: 4 x 16 bit
-    uint32_t w0, w1;
-    asm volatile(DACSR_PAIR_PRED "ld.global.cs.v2.b32 {%0, %1}, [%2];\n\t}"
-                 : "=r"(w0), "=r"(w1) : "l"(p), "r"(static_cast<unsigned>(pred)));
-    if constexpr (std::is_same<T, int16_t>::value) {
-      o[0] = static_cast<int>(static_cast<int16_t>(w0 & 0xffffu));
-      o[1] = static_cast<int>(w0) >> 16;
-      o[2] = static_cast<int>(static_cast<int16_t>(w1 & 0xffffu));
-      o[3] = static_cast<int>(w1) >> 16;
-    } else if constexpr (std::is_same<T, __half>::value) {
-      o[0] = __ushort_as_half(static_cast<unsigned short>(w0 & 0xffffu));
-      o[1] = __ushort_as_half(static_cast<unsigned short>(w0 >> 16));
-      o[2] = __ushort_as_half(static_cast<unsigned short>(w1 & 0xffffu));
-      o[3] = __ushort_as_half(static_cast<unsigned short>(w1 >> 16));
-    } else {
-      o[0] = __ushort_as_bfloat16(static_cast<unsigned short>(w0 & 0xffffu));
-      o[1] = __ushort_as_bfloat16(static_cast<unsigned short>(w0 >> 16));
-      o[2] = __ushort_as_bfloat16(static_cast<unsigned short>(w1 & 0xffffu));
-      o[3] = __ushort_as_bfloat16(static_cast<unsigned short>(w1 >> 16));
-    }
-  } else {  // int8: 4 bytes
-    const uint32_t w = pair_ld_cs_b32(p, pred);
-    o[0] = static_cast<int>(static_cast<int8_t>(w & 0xffu));
-    o[1] = static_cast<int>(static_cast<int8_t>((w >> 8) & 0xffu));
-    o[2] = static_cast<int>(static_cast<int8_t>((w >> 16) & 0xffu));
-    o[3] = static_cast<int>(static_cast<int8_t>(w >> 24));
-  }
+template <class T>
+__device__ __forceinline__ typename std::enable_if<sizeof(T) == 2>::type pair_ld_cs(
+    const T* p, bool pred, uint32_t* w) {
+  asm volatile(DACSR_ONE_PRED "ld.global.cs.b32 %0, [%1];\n\t}"
+               : "=r"(w[0]) : "l"(p), "r"(static_cast<unsigned>(pred)));
+}
+__device__ __forceinline__ void pair_ld_cs(const int8_t* p, bool pred, uint32_t* w) {
+  asm volatile(DACSR_ONE_PRED "ld.global.cs.u16 %0, [%1];\n\t}"
+               : "=r"(w[0]) : "l"(p), "r"(static_cast<unsigned>(pred)));
 }
 #undef DACSR_PAIR_PRED
+#undef DACSR_ONE_PRED
+
+// element K (0 or 1) of a loaded pair, as the fold consumes it
+template <class T, int K>
+__device__ __forceinline__ auto pair_elem(const typename PairReg<T>::W* w) {
+  if constexpr (!PairReg<T>::kPacked) {
+    return w[K];
+  } else if constexpr (std::is_same<T, int16_t>::value) {
+    int v;
+    if constexpr (K == 0)
+      asm volatile("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(v) : "r"(w[0]));
+    else
+      asm volatile("shr.s32 %0, %1, 16;" : "=r"(v) : "r"(w[0]));
+    return v;
+  } else if constexpr (std::is_same<T, int8_t>::value) {
+    int v;
+    asm volatile("bfe.s32 %0, %1, %2, 8;" : "=r"(v) : "r"(w[0]), "n"(8 * K));
+    return v;
+  } else {  // __half / __nv_bfloat16 bits
+    unsigned short h;
+    if constexpr (K == 0)
+      asm volatile("{\n\t.reg .b16 t;\n\tmov.b32 {%0, t}, %1;\n\t}" : "=h"(h) : "r"(w[0]));
+    else
+      asm volatile("{\n\t.reg .b16 t;\n\tmov.b32 {t, %0}, %1;\n\t}" : "=h"(h) : "r"(w[0]));
+    if constexpr (std::is_same<T, __half>::value)
+      return __ushort_as_half(h);
+    else
+      return __ushort_as_bfloat16(h);
+  }
+}
 
 // acc += p (round to nearest) when pred, as one predicated DADD
 __device__ __forceinline__ void dadd_if(double& acc, double p, bool pred) {
@@ -251,7 +240,7 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
   using OT = typename std::conditional<sizeof(CI) == 8, int64_t, int>::type;
   constexpr int U = DACSR_TILED_BATCH;
   constexpr int G = DACSR_TILED_G;
-  static_assert(U % G == 0, "batch must be whole step groups");
+  static_assert(G == 2 && U % G == 0, "the kernel folds pair steps, whole pairs per batch");
   extern __shared__ __align__(128) unsigned char dsm[];
   VT* const xs = reinterpret_cast<VT*>(dsm);
   const size_t xstride = tiled_xbuf_bytes<VT>(xbuf) / sizeof(VT);
@@ -463,7 +452,10 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         // ballots, then every operator load of the batch issued (G-entry
         // vector loads, predicated asm, program order)
         constexpr int UP = U / G;
-        auto load_batch = [&](int q0, OT* off, VT* val) {
+        using OW = typename PairReg<CI>::W;
+        using VW = typename PairReg<VT>::W;
+        constexpr int OK = PairReg<CI>::kWords, VK = PairReg<VT>::kWords;
+        auto load_batch = [&](int q0, OW* off, VW* val) {
 #pragma unroll
           for (int u = 0; u < UP; ++u) {
             const bool act = G * (q0 + u) < total;
@@ -471,16 +463,20 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
             const uint32_t o = lp + G * __popc(msk & below);
             lp += G * __popc(msk);
             DACSR_CHECK(!act || pos + o + G - 1 < ta.total);
-            if constexpr (G == 2) {
-              pair_ld_cs(elem_addr_u32(ct, o), act, off[2 * u], off[2 * u + 1]);
-              pair_ld_cs(elem_addr_u32(vt, o), act, val[2 * u], val[2 * u + 1]);
-            } else {
-              quad_ld_cs(elem_addr_u32(ct, o), act, off + 4 * u);
-              quad_ld_cs(elem_addr_u32(vt, o), act, val + 4 * u);
-            }
+            pair_ld_cs(elem_addr_u32(ct, o), act, off + OK * u);
+            pair_ld_cs(elem_addr_u32(vt, o), act, val + VK * u);
           }
         };
-        auto fold_batch = [&](int k0, const OT* off, const VT* val) {
+        // element u of a batch (u even: first of pair u / 2); u is a
+        // constant after unrolling, so one branch remains
+        auto off_at = [&](const OW* off, int u) -> OT {
+          return static_cast<OT>(u & 1 ? pair_elem<CI, 1>(off + OK * (u / 2))
+                                       : pair_elem<CI, 0>(off + OK * (u / 2)));
+        };
+        auto val_at = [&](const VW* val, int u) -> VT {
+          return u & 1 ? pair_elem<VT, 1>(val + VK * (u / 2)) : pair_elem<VT, 0>(val + VK * (u / 2));
+        };
+        auto fold_batch = [&](int k0, const OW* off, const VW* val) {
           const int left = total - k0;  // steps of this lane left in the tile
           if constexpr (KIND == DACSR_KIND_DA) {
             // the row of each step from the counts alone (no dependence on
@@ -509,9 +505,9 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
                 acc_a = wab + (xrs[u] - xg) * static_cast<uint32_t>(8 / sizeof(VT));
                 acc = lds_f64(acc_a);
               }
-              const uint32_t xa = xrs[u] + static_cast<uint32_t>(static_cast<int>(off[u]) * static_cast<int>(sizeof(VT)));
+              const uint32_t xa = xrs[u] + static_cast<uint32_t>(static_cast<int>(off_at(off, u)) * static_cast<int>(sizeof(VT)));
               DACSR_CHECK(!(u < left) || (xa >= xsa && xa < xsa + xbuf * sizeof(VT)));
-              if (u < left) dadd_if(acc, product(val[u], lds_val<VT>(xa)), true);
+              if (u < left) dadd_if(acc, product(val_at(val, u), lds_val<VT>(xa)), true);
             }
           } else {
 #pragma unroll
@@ -526,16 +522,16 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
                                     (lane ^ static_cast<uint32_t>((mw >> (4 * j)) & 15u)));
                 acc = lds_f64(acc_a);
               }
-              const uint32_t xa = xc + static_cast<uint32_t>(off[u] * static_cast<OT>(sizeof(VT)));
+              const uint32_t xa = xc + static_cast<uint32_t>(off_at(off, u) * static_cast<OT>(sizeof(VT)));
               DACSR_CHECK(!act || (xa >= xsa && xa < xsa + xbuf * sizeof(VT)));
-              if (act) dadd_if(acc, product(val[u], lds_val<VT>(xa)), true);
+              if (act) dadd_if(acc, product(val_at(val, u), lds_val<VT>(xa)), true);
               --rem;
             }
           }
         };
         // two batches in flight: batch i+1's loads are issued before batch i folds
-        OT offA[U], offB[U];
-        VT valA[U], valB[U];
+        OW offA[OK * U / 2], offB[OK * U / 2];
+        VW valA[VK * U / 2], valB[VK * U / 2];
         int k0 = 0;
         if (kmax > 0) load_batch(0, offA, valA);
         while (k0 < kmax) {
