@@ -149,11 +149,13 @@ typedef struct {
  * tile_lo[g] .. tile_lo[g] + (cnt_ptr[g+1] - cnt_ptr[g]) - 1; its k-th tile
  * is block b = cnt_ptr[g] + k.  In block b lane l folds, for j = 0..15, row
  * slot 32j + (l ^ m_j), m_j = nibble j of masks[b] (a per-tile lane remap
- * that evens out the lanes' list lengths); counts[b * 32 + l] holds 16
- * nibbles, nibble j = the entries of that row whose column falls in the
- * tile (0..15).
+ * that evens out the lanes' list lengths), in the order order[b * 32 + l]
+ * gives: nibble k = the row slot j of its k-th row (an order chosen to
+ * spread the shared-memory banks); nibble k of counts[b * 32 + l] = the
+ * entries of that row whose column falls in the tile (1..15; rows without
+ * entries in the tile are not listed, their nibbles 0).
  * The group's entries start at ent_ptr[g], tile after tile.  Inside a tile,
- * lane l's entries (its rows j = 0..15 in order, each row's entries in
+ * lane l's entries (its rows in that order, each row's entries in
  * column order) form a list L_l, stored in steps of G = step_group
  * entries: entries Gq .. Gq+G-1 of L_l sit at tile_base + G * (sum_{q' < q}
  * |{l' : |L_l'| > Gq'}| + |{l' < l : |L_l'| > Gq}|) (a list whose length
@@ -186,6 +188,7 @@ typedef struct {
   int64_t n_ovf;
   const int64_t* ovf_rows;  /* n_ovf, ascending                             */
   const uint64_t* masks;    /* nblocks: lane remap nibbles of each block     */
+  const uint64_t* order;    /* nblocks * 32: row order nibbles               */
 } dacsr_tiles_t;
 
 /* dacsr_plan_t.flags: the SLICED kernels skip the L2 bulk prefetch of the

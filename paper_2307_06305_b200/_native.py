@@ -97,7 +97,8 @@ class Tiles(ctypes.Structure):
                 ("tile_lo", ctypes.c_void_p), ("counts", ctypes.c_void_p),
                 ("skip", ctypes.c_void_p), ("inner", ctypes.c_void_p),
                 ("values", ctypes.c_void_p), ("n_ovf", ctypes.c_int64),
-                ("ovf_rows", ctypes.c_void_p), ("masks", ctypes.c_void_p)]
+                ("ovf_rows", ctypes.c_void_p), ("masks", ctypes.c_void_p),
+                ("order", ctypes.c_void_p)]
 
 
 def typed_kernel_names():

@@ -1384,7 +1384,7 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
           td->tile_cols > 65536 || (td->tile_cols & 15) ||
           td->ngroups != (td->row_end - td->row_start + 511) / 512 ||
           (td->ngroups > 0 && (!td->ent_ptr || !td->cnt_ptr || !td->tile_lo || !td->skip)) ||
-          (td->nblocks > 0 && (!td->counts || !td->masks)) || (td->total > 0 && (!td->inner || !td->values)) ||
+          (td->nblocks > 0 && (!td->counts || !td->order || !td->masks)) || (td->total > 0 && (!td->inner || !td->values)) ||
           (td->n_ovf > 0 && !td->ovf_rows) || (a->nnz > 0 && (!a->colids || !a->values)))
         return DACSR_ERR_PLAN;
       if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
@@ -1408,7 +1408,7 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       const int64_t grid = std::max<int64_t>(
           1, std::min<int64_t>(std::max<int64_t>(nchunks, (td->n_ovf + kTileWarps - 1) / kTileWarps),
                                static_cast<int64_t>(sms) * per_sm));
-      TileArgs<CI, VT> ta{td->ent_ptr, td->cnt_ptr, td->tile_lo, td->counts, td->masks, td->skip,
+      TileArgs<CI, VT> ta{td->ent_ptr, td->cnt_ptr, td->tile_lo, td->counts, td->order, td->masks, td->skip,
                           static_cast<const CI*>(td->inner), static_cast<const VT*>(td->values),
                           td->ovf_rows, td->row_start, td->col0, td->cmax, td->total, td->n_ovf,
                           td->tile_cols};

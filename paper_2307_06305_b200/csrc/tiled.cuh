@@ -45,6 +45,7 @@ struct TileArgs {
   const int64_t* __restrict__ cnt_ptr;
   const int32_t* __restrict__ tile_lo;
   const uint64_t* __restrict__ counts;
+  const uint64_t* __restrict__ order;
   const uint64_t* __restrict__ masks;
   const uint16_t* __restrict__ skip;
   const CI* __restrict__ ci;
@@ -216,16 +217,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   }
 }
 
-// bit j = nibble j of v is non-zero
-__device__ __forceinline__ uint32_t nonzero_nibbles(uint64_t v) {
-  uint64_t t = v | (v >> 1);
-  t = (t | (t >> 2)) & 0x1111111111111111ull;  // bit 4j
-  t = (t | (t >> 3)) & 0x0303030303030303ull;  // byte k: bits 0, 1
-  t = (t | (t >> 6)) & 0x000F000F000F000Full;  // 16-bit half k: bits 0..3
-  t = (t | (t >> 12)) & 0x000000FF000000FFull;
-  return static_cast<uint32_t>((t | (t >> 24)) & 0xFFFFu);
-}
-
 // Group metadata of the chunk, one group per lane (lanes < kTileWarps),
 // loaded a chunk ahead.
 struct ChunkMeta {
@@ -360,11 +351,13 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         __reduce_add_sync(0xffffffffu, static_cast<unsigned>((nibble_sum(w) + G - 1) / G * G)));
   };
   // count words and lane remap words of a block: (counts, masks)
-  uint64_t ncn0 = 0, ncn1 = 0, nmw0 = 0, nmw1 = 0;
+  // and row order words (one tile ahead: the fold alone reads them)
+  uint64_t ncn0 = 0, ncn1 = 0, nmw0 = 0, nmw1 = 0, now0 = 0;
   auto load_first_counts = [&](const ChunkMeta& q2) {
     const int64_t c0 = __shfl_sync(0xffffffffu, q2.cnt0, warp);
     const int64_t c1 = __shfl_sync(0xffffffffu, q2.cnt1, warp);
     ncn0 = c1 > c0 ? ldg(ta.counts + c0 * 32 + lane) : 0;
+    now0 = c1 > c0 ? ldg(ta.order + c0 * 32 + lane) : 0;
     nmw0 = c1 > c0 ? ldg(ta.masks + c0) : 0;
     ncn1 = c1 > c0 + 1 ? ldg(ta.counts + (c0 + 1) * 32 + lane) : 0;
     nmw1 = c1 > c0 + 1 ? ldg(ta.masks + c0 + 1) : 0;
@@ -383,7 +376,7 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
     int64_t pos = __shfl_sync(0xffffffffu, q.ent, warp);
 #pragma unroll
     for (int j = 0; j < kTileRows; ++j) sts_f64(wa + 256u * j, 0.0);
-    uint64_t cn0 = ncn0, cn1 = ncn1, mw0 = nmw0, mw1 = nmw1;
+    uint64_t cn0 = ncn0, cn1 = ncn1, mw0 = nmw0, mw1 = nmw1, ow0 = now0;
     // the operator segment of the group's first tile into L2 now, every
     // later one a tile ahead of its fold (bulk prefetch; measured: without
     // it C3 runs 11 % slower, two tiles ahead 4 % slower)
@@ -406,11 +399,13 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
     for (int64_t t = tlo; t <= thi; ++t) {
       const int64_t k = t - gtlo;
       const bool mine = has && k >= 0 && k < gnt;
-      uint64_t cur = 0, mw = 0;
+      uint64_t cur = 0, mw = 0, ow = 0;
       int total = 0;
       if (mine) {
         cur = cn0;
         mw = mw0;
+        ow = ow0;
+        ow0 = k + 1 < gnt ? ldg(ta.order + (cbase + k + 1) * 32 + lane) : 0;
         cn0 = cn1;
         mw0 = mw1;
         cn1 = k + 2 < gnt ? ldg(ta.counts + (cbase + k + 2) * 32 + lane) : 0;
@@ -435,8 +430,9 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         const uint32_t xc = xsa - xoff;
         const uint32_t xg = xc + grow_b;
         const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
-        // rows of this tile with entries (bit j), consumed in order
-        uint32_t nz = nonzero_nibbles(cur);
+        // the lane's rows in fold order: nibble kq / 4 of ow (row slot j)
+        // and of cur (its entries in the tile)
+        uint32_t kq = 0;
         int rem = 0;
         uint32_t acc_a = wa + 32u * 8u * kTileRows;  // dummy slot
         uint32_t xr = xg;
@@ -487,12 +483,11 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const bool sw = u < left && rem == 0;
-              const int jn = (__ffs(nz) - 1) & 15;
-              const uint32_t nz2 = nz & (nz - 1);
-              const int rem2 = static_cast<int>((cur >> (4 * jn)) & 15u);
-              const uint32_t slot = (static_cast<uint32_t>(jn) << 5) |
-                                    (lane ^ static_cast<uint32_t>((mw >> (4 * jn)) & 15u));
-              nz = sw ? nz2 : nz;
+              const uint32_t sh = kq & 63u;  // 64 only once every row is done (sw false)
+              const uint32_t jn = static_cast<uint32_t>(ow >> sh) & 15u;
+              const int rem2 = static_cast<int>((cur >> sh) & 15u);
+              const uint32_t slot = (jn << 5) | (lane ^ static_cast<uint32_t>((mw >> (4 * jn)) & 15u));
+              kq = sw ? kq + 4u : kq;
               rem = (sw ? rem2 : rem) - 1;
               xr = sw ? xg + slot * static_cast<uint32_t>(sizeof(VT)) : xr;
               swm |= sw ? 1u << u : 0u;
@@ -515,10 +510,10 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
               const bool act = u < left;  // once false, false for the rest of the tile
               if (act && rem == 0) {  // this lane's next row of the tile
                 sts_f64(acc_a, acc);
-                const int j = __ffs(nz) - 1;
-                nz &= nz - 1;
-                rem = static_cast<int>((cur >> (4 * j)) & 15u);
-                acc_a = wab + 8u * ((static_cast<uint32_t>(j) << 5) |
+                const uint32_t j = static_cast<uint32_t>(ow >> kq) & 15u;
+                rem = static_cast<int>((cur >> kq) & 15u);
+                kq += 4u;
+                acc_a = wab + 8u * ((j << 5) |
                                     (lane ^ static_cast<uint32_t>((mw >> (4 * j)) & 15u)));
                 acc = lds_f64(acc_a);
               }

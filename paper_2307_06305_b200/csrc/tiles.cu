@@ -11,8 +11,10 @@
 //   group g (512 rows, row slot 32j + l)
 //     tile t (tile_lo[g] ..):  mask        — 16 nibbles m_j: lane l folds
 //                                           row slot 32j + (l ^ m_j)
-//                              counts[32]  — lane l: 16 nibbles (entries of
-//                                           its row j inside the tile)
+//                              order[32]   — lane l: nibble k = j of the
+//                                           k-th row it folds in the tile
+//                              counts[32]  — lane l: nibble k = entries of
+//                                           that row inside the tile
 //                              entries     — lane lists L_l stored in pair
 //                                           steps (pair step q: entries 2q,
 //                                           2q + 1 of every lane whose list
@@ -107,6 +109,83 @@ __device__ __forceinline__ uint64_t balance_lanes(const int (&c)[kRowsPerLane], 
   }
   total = tot;
   return mw;
+}
+
+// Row order of one tile, chosen for the shared-memory banks.  At each step
+// a lane either continues its row or starts its next one; the starting
+// lanes pick, one lane per half warp at a time, the not yet started row
+// whose first x gather and whose accumulator swap (store + load) collide
+// least with the bank pairs the half warp already hits at that step
+// (cost = x hits + 2 x accumulator hits, ties to the lowest j).  Returns
+// the order word (nibble k = row slot j of the lane's k-th row) and the
+// counts word in that order.  Every row's entries stay consecutive and in
+// column order, so any order folds every row in the naive order.
+template <int KIND, class CI, class VB>
+__device__ void order_rows(const CI* __restrict__ ci, const int64_t (&src)[kRowsPerLane],
+                           const int (&nr)[kRowsPerLane], uint64_t mw, int64_t row_base,
+                           int64_t tstart, int total, int kmax, uint64_t& ow, uint64_t& cw) {
+  const int lane = threadIdx.x & 31;
+  // bank pair (8-byte units, 16 per half warp) of a gather at column c
+  auto xkey = [&](int64_t c) {
+    return static_cast<int>(((c - tstart) * static_cast<int64_t>(sizeof(VB)) >> 3) & 15);
+  };
+  auto row_of = [&](int j) {
+    return row_base + 32 * j + (lane ^ static_cast<int>((mw >> (4 * j)) & 15u));
+  };
+  uint64_t fk = 0;    // nibble j: x bank pair of row j's first entry
+  unsigned left = 0;  // rows not started (bit j)
+  for (int j = 0; j < kRowsPerLane; ++j)
+    if (nr[j] > 0) {
+      left |= 1u << j;
+      fk |= static_cast<uint64_t>(xkey(entry_col<KIND>(row_of(j), ci[src[j]]))) << (4 * j);
+    }
+  int rem = 0, k = 0;
+  int64_t p = 0, rowc = 0;
+  ow = cw = 0;
+  for (int st = 0; st < kmax; ++st) {
+    const bool act = st < total;
+    const bool sw = act && rem == 0;
+    // bank pairs hit by the lanes that continue a row (per half warp;
+    // 4-bit counters, a saturated one only skews the heuristic)
+    uint64_t xo = act && !sw ? 1ull << (4 * xkey(entry_col<KIND>(rowc, ci[p]))) : 0ull;
+    for (int o = 8; o > 0; o >>= 1) xo += __shfl_xor_sync(0xffffffffu, xo, o);
+    uint64_t ao = 0;
+    const unsigned swm = __ballot_sync(0xffffffffu, sw);
+    for (unsigned qm = (swm | (swm >> 16)) & 0xffffu; qm; qm &= qm - 1) {
+      const int q = __ffs(qm) - 1;
+      const bool me = sw && (lane & 15) == q;
+      uint64_t add_x = 0, add_a = 0;
+      if (me) {
+        int best = INT_MAX, pick = 0;
+        for (unsigned m = left; m; m &= m - 1) {
+          const int j = __ffs(m) - 1;
+          const int ak = (lane ^ static_cast<int>((mw >> (4 * j)) & 15u)) & 15;
+          const int cost = 2 * static_cast<int>((ao >> (4 * ak)) & 15u) +
+                           static_cast<int>((xo >> (4 * ((fk >> (4 * j)) & 15u))) & 15u);
+          if (cost < best) {
+            best = cost;
+            pick = j;
+          }
+        }
+        left &= ~(1u << pick);
+        ow |= static_cast<uint64_t>(pick) << (4 * k);
+        cw |= static_cast<uint64_t>(nr[pick]) << (4 * k);
+        ++k;
+        rem = nr[pick];
+        p = src[pick];
+        rowc = row_of(pick);
+        add_x = 1ull << (4 * ((fk >> (4 * pick)) & 15u));
+        add_a = 1ull << (4 * ((lane ^ static_cast<int>((mw >> (4 * pick)) & 15u)) & 15));
+      }
+      const int from = (lane & 16) | q;
+      xo += __shfl_sync(0xffffffffu, add_x, from);
+      ao += __shfl_sync(0xffffffffu, add_a, from);
+    }
+    if (act) {
+      --rem;
+      ++p;
+    }
+  }
 }
 
 struct TileGeom {
@@ -207,7 +286,8 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
     TileGeom geo, int64_t ngroups, const int64_t* __restrict__ ent_ptr,
     const int64_t* __restrict__ cnt_ptr, const int32_t* __restrict__ tile_lo,
     const uint16_t* __restrict__ skip, const int64_t* __restrict__ ovf_ptr,
-    uint64_t* __restrict__ counts, uint64_t* __restrict__ masks, IT* __restrict__ t_inner,
+    uint64_t* __restrict__ counts, uint64_t* __restrict__ order, uint64_t* __restrict__ masks,
+    IT* __restrict__ t_inner,
     VB* __restrict__ t_values, int64_t* __restrict__ ovf_rows) {
   const int lane = threadIdx.x & 31;
   const unsigned below = (1u << lane) - 1u;
@@ -253,24 +333,26 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
       // the rows this lane folds: slot 32j + (lane ^ m_j)
       int64_t src[kRowsPerLane];
       int nr[kRowsPerLane];
-      uint64_t nib = 0;
 #pragma unroll
       for (int j = 0; j < kRowsPerLane; ++j) {
         const int from = lane ^ static_cast<int>((mw >> (4 * j)) & 15u);
         nr[j] = __shfl_sync(0xffffffffu, n[j], from);
         src[j] = __shfl_sync(0xffffffffu, cur[j], from);
-        nib |= static_cast<uint64_t>(nr[j]) << (4 * j);
       }
-      counts[(cnt_ptr[g] + k) * 32 + lane] = nib;
-      if (lane == 0) masks[cnt_ptr[g] + k] = mw;
       const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
-      int j = 0, used = 0;
+      uint64_t ow, cw;
+      order_rows<KIND, CI, VB>(ci, src, nr, mw, geo.rs + kGroupRows * g, geo.col0 + t * geo.T, total,
+                               kmax, ow, cw);
+      counts[(cnt_ptr[g] + k) * 32 + lane] = cw;
+      order[(cnt_ptr[g] + k) * 32 + lane] = ow;
+      if (lane == 0) masks[cnt_ptr[g] + k] = mw;
+      int kk = 0, used = 0;
       auto next_src = [&]() {  // this lane's next list entry
-        while (used == nr[j]) {
-          ++j;
+        while (used == static_cast<int>((cw >> (4 * kk)) & 15u)) {
+          ++kk;
           used = 0;
         }
-        return src[j] + used++;
+        return src[(ow >> (4 * kk)) & 15u] + used++;
       };
       for (int s = 0; s < kmax; s += geo.G) {  // step group: list entries s .. s + G - 1
         const bool act = s < total;
@@ -411,7 +493,7 @@ int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int6
                      void* stream) {
   if (!geometry_ok(a, t) || !ovf_ptr ||
       (t->ngroups > 0 && (!t->ent_ptr || !t->cnt_ptr || !t->tile_lo || !t->skip)) ||
-      (t->nblocks > 0 && (!t->counts || !t->masks)) ||
+      (t->nblocks > 0 && (!t->counts || !t->order || !t->masks)) ||
       (t->total > 0 && (!t->inner || !t->values)) || (t->n_ovf > 0 && !t->ovf_rows))
     return DACSR_ERR_ARG;
   if (t->ngroups == 0) return DACSR_OK;
@@ -427,7 +509,8 @@ int dacsr_tiles_fill(const dacsr_matrix_t* a, const dacsr_tiles_t* t, const int6
     tiles_fill_kernel<KIND, RP, CI, IT, VB><<<g, 128, 0, st>>>(
         static_cast<const RP*>(a->rowptr), static_cast<const CI*>(a->colids),
         static_cast<const VB*>(a->values), geo, t->ngroups, t->ent_ptr, t->cnt_ptr, t->tile_lo,
-        t->skip, ovf_ptr, const_cast<uint64_t*>(t->counts), const_cast<uint64_t*>(t->masks),
+        t->skip, ovf_ptr, const_cast<uint64_t*>(t->counts), const_cast<uint64_t*>(t->order),
+        const_cast<uint64_t*>(t->masks),
         static_cast<IT*>(const_cast<void*>(t->inner)), static_cast<VB*>(const_cast<void*>(t->values)),
         const_cast<int64_t*>(t->ovf_rows));
     return check_launch("tiles_fill_kernel");

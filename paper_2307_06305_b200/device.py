@@ -364,7 +364,7 @@ class DeviceMatrix:
             tl = _native.Tiles(rs, re, ng, cmin, cmax, tile_cols, L.dacsr_tiles_step_group(), 0, 0,
                                None, None,
                                tile_lo.data_ptr(), None, skip.data_ptr(), None, None, 0, None,
-                               None)
+                               None, None)
             cnt = torch.zeros(3, max(ng, 1), dtype=torch.int32, device=dev)
             _native.check(L.dacsr_tiles_count(ctypes.byref(self.desc), ctypes.byref(tl),
                                                vp(cnt[0]), vp(cnt[1]), vp(cnt[2]), sp),
@@ -376,13 +376,14 @@ class DeviceMatrix:
             nblocks, total, n_ovf = (int(v) for v in ptrs[:, ng].tolist())
             counts = torch.empty(max(32 * nblocks, 1), dtype=torch.int64, device=dev)  # uint64 bits
             masks = torch.empty(max(nblocks, 1), dtype=torch.int64, device=dev)  # uint64 bits
+            order = torch.empty(max(32 * nblocks, 1), dtype=torch.int64, device=dev)  # uint64 bits
             inner = torch.zeros(total + 16, dtype=self.colids.dtype, device=dev)
             values = torch.zeros(total + 16, dtype=self.values.dtype, device=dev)
             ovf_rows = torch.empty(max(n_ovf, 1), dtype=torch.int64, device=dev)
             tl.total, tl.nblocks, tl.n_ovf = total, nblocks, n_ovf
             tl.cnt_ptr, tl.ent_ptr = ptrs[0].data_ptr(), ptrs[1].data_ptr()
             tl.counts, tl.inner, tl.values = counts.data_ptr(), inner.data_ptr(), values.data_ptr()
-            tl.ovf_rows, tl.masks = ovf_rows.data_ptr(), masks.data_ptr()
+            tl.ovf_rows, tl.masks, tl.order = ovf_rows.data_ptr(), masks.data_ptr(), order.data_ptr()
             _native.check(L.dacsr_tiles_fill(ctypes.byref(self.desc), ctypes.byref(tl),
                                               vp(ptrs[2]), sp), "dacsr_tiles_fill")
             _sync(stream)
@@ -391,7 +392,7 @@ class DeviceMatrix:
         plan.slices = self._sliced[0].slices if self._sliced is not None else None
         plan.tiles = ctypes.addressof(tl)
         tensors = {"ptrs": ptrs, "tile_lo": tile_lo, "skip": skip, "counts": counts,
-                   "masks": masks, "inner": inner, "values": values, "ovf_rows": ovf_rows}
+                   "masks": masks, "order": order, "inner": inner, "values": values, "ovf_rows": ovf_rows}
         self._tiled = (plan, tl, tensors)
         self._invalidate_launches()
         return plan
@@ -406,7 +407,7 @@ class DeviceMatrix:
                 "cmax": tl.cmax,
                 "groups": tl.ngroups, "tile_blocks": tl.nblocks,
                 "tiles_per_group": tl.nblocks / ng, "entries": tl.total, "n_ovf": tl.n_ovf,
-                "count_bytes_per_row": 8 * tl.nblocks * 32 / max(1, tl.row_end - tl.row_start),
+                "count_bytes_per_row": (16 * 32 + 8) * tl.nblocks / max(1, tl.row_end - tl.row_start),
                 "bytes": sum(t.numel() * t.element_size() for t in tensors.values())}
 
     def _invalidate_launches(self):

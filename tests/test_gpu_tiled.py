@@ -32,16 +32,32 @@ def untile(dm):
     cnt_ptr, ent_ptr = ptrs[0], ptrs[1]
     tile_lo = t["tile_lo"].cpu().numpy()
     counts = t["counts"].cpu().numpy().view(np.uint64)
+    order = t["order"].cpu().numpy().view(np.uint64)
     masks = t["masks"].cpu().numpy().view(np.uint64)
     inner, vals = t["inner"].cpu().numpy(), t["values"].cpu().numpy()
     rows = {}
     for g in range(tl.ngroups):
         pos = int(ent_ptr[g])
         for k in range(int(cnt_ptr[g + 1] - cnt_ptr[g])):
-            nib = counts[(cnt_ptr[g] + k) * 32:(cnt_ptr[g] + k + 1) * 32]
-            n = [[(int(nib[l]) >> (4 * j)) & 15 for j in range(16)] for l in range(32)]
-            mw = int(masks[cnt_ptr[g] + k])
-            tot = [sum(v) for v in n]
+            b = int(cnt_ptr[g]) + k
+            cw = [int(w) for w in counts[b * 32:(b + 1) * 32]]
+            ow = [int(w) for w in order[b * 32:(b + 1) * 32]]
+            mw = int(masks[b])
+            # lane l: its rows in fold order (k-th: slot j = nibble k of ow,
+            # n = nibble k of cw; the list ends at the first n = 0)
+            seq = []
+            for l in range(32):
+                s_l = []
+                for q in range(16):
+                    n = (cw[l] >> (4 * q)) & 15
+                    if n == 0:
+                        assert cw[l] >> (4 * q) == 0
+                        break
+                    s_l.append(((ow[l] >> (4 * q)) & 15, n))
+                js = [j for j, _ in s_l]
+                assert len(set(js)) == len(js)
+                seq.append(s_l)
+            tot = [sum(n for _, n in s_l) for s_l in seq]
             lists = [[] for _ in range(32)]
             G = tl.step_group
             for q in range((max(tot) + G - 1) // G):
@@ -51,9 +67,9 @@ def untile(dm):
                         pos += G
             for l in range(32):
                 slots = iter(lists[l])
-                for j in range(16):
+                for j, n in seq[l]:
                     r = tl.row_start + 512 * g + 32 * j + (l ^ ((mw >> (4 * j)) & 15))
-                    for _ in range(n[l][j]):
+                    for _ in range(n):
                         p = next(slots)
                         rows.setdefault(r, []).append((int(tile_lo[g]) + k, inner[p], vals[p]))
         assert pos == ent_ptr[g + 1]
