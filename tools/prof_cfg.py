@@ -35,11 +35,15 @@ elif c == "c3":
     from paper_2307_06305_b200.gen import banded_device, normal_vector
     mats = banded_device("c3", dev)
     x = normal_vector(mats["da"].ncols, 17, dev)
+elif c == "c5slab":  # one 8-GPU rank's share of C5: rows [0, 2^25) (rank 0's slab)
+    from paper_2307_06305_b200.gen import banded_device, normal_vector
+    mats = banded_device("c5", dev, kinds=tuple(args.kinds.split(",")), r0=0, r1=1 << 25)
+    x = normal_vector(1 << 28, 21, dev)
 else:
     dt = np.float32 if c == "c2f32" else np.float64
     csr = laplacian_2d(1024, dt) if c == "c1" else laplacian_3d(128, dt)
     xh = uniform_x(csr.ncols, 1).astype(dt)
-if c != "c3":
+if c not in ("c3", "c5slab"):
     mats = {"csr": DeviceMatrix.from_host(csr), "da": DeviceMatrix.from_host(dg.to_dacsr(csr, 16))}
     x = torch.from_numpy(xh).to(dev)
     if c == "c2bf16":
