@@ -114,17 +114,30 @@ __device__ __forceinline__ uint64_t balance_lanes(const int (&c)[kRowsPerLane], 
 // Row order of one tile, chosen for the shared-memory banks.  At each step
 // a lane either continues its row or starts its next one; the starting
 // lanes pick, one lane per half warp at a time, the not yet started row
-// whose first x gather and whose accumulator swap (store + load) collide
-// least with the bank pairs the half warp already hits at that step
-// (cost = x hits + 2 x accumulator hits, ties to the lowest j).  Returns
-// the order word (nibble k = row slot j of the lane's k-th row) and the
-// counts word in that order.  Every row's entries stay consecutive and in
-// column order, so any order folds every row in the naive order.
+// whose bank pairs collide least with the rows already placed: its x
+// gathers at this and the following steps, its accumulator load now and
+// its accumulator store at the step its successor starts (cost = the
+// number of lanes of the half warp already on each of those bank pairs;
+// ties to the lowest j).  Returns the order word (nibble k = row slot j of
+// the lane's k-th row) and the counts word in that order.  Every row's
+// entries stay consecutive and in column order, so any order folds every
+// row in the naive order.
+constexpr int kOrderSteps = kRowsPerLane * 15 + 16;  // longest list + a row
+struct OrderScratch {  // per warp: 4-bit counters per (half, step, bank pair)
+  uint64_t x[2][kOrderSteps];   // x gathers
+  uint64_t st[2][kOrderSteps];  // accumulator stores
+};
+__device__ __forceinline__ int occ_get(uint64_t w, int b) { return static_cast<int>((w >> (4 * b)) & 15u); }
+__device__ __forceinline__ uint64_t occ_add(uint64_t w, int b) {  // saturating
+  return occ_get(w, b) == 15 ? w : w + (1ull << (4 * b));
+}
 template <int KIND, class CI, class VB>
 __device__ void order_rows(const CI* __restrict__ ci, const int64_t (&src)[kRowsPerLane],
                            const int (&nr)[kRowsPerLane], uint64_t mw, int64_t row_base,
-                           int64_t tstart, int total, int kmax, uint64_t& ow, uint64_t& cw) {
+                           int64_t tstart, int total, int kmax, OrderScratch& sc, uint64_t& ow,
+                           uint64_t& cw) {
   const int lane = threadIdx.x & 31;
+  const int h = lane >> 4;
   // bank pair (8-byte units, 16 per half warp) of a gather at column c
   auto xkey = [&](int64_t c) {
     return static_cast<int>(((c - tstart) * static_cast<int64_t>(sizeof(VB)) >> 3) & 15);
@@ -132,36 +145,33 @@ __device__ void order_rows(const CI* __restrict__ ci, const int64_t (&src)[kRows
   auto row_of = [&](int j) {
     return row_base + 32 * j + (lane ^ static_cast<int>((mw >> (4 * j)) & 15u));
   };
-  uint64_t fk = 0;    // nibble j: x bank pair of row j's first entry
+  for (int i = lane; i < 2 * (kmax + 16); i += 32) {
+    sc.x[i & 1][i >> 1] = 0;
+    sc.st[i & 1][i >> 1] = 0;
+  }
+  __syncwarp();
   unsigned left = 0;  // rows not started (bit j)
   for (int j = 0; j < kRowsPerLane; ++j)
-    if (nr[j] > 0) {
-      left |= 1u << j;
-      fk |= static_cast<uint64_t>(xkey(entry_col<KIND>(row_of(j), ci[src[j]]))) << (4 * j);
-    }
+    if (nr[j] > 0) left |= 1u << j;
   int rem = 0, k = 0;
-  int64_t p = 0, rowc = 0;
   ow = cw = 0;
-  for (int st = 0; st < kmax; ++st) {
-    const bool act = st < total;
-    const bool sw = act && rem == 0;
-    // bank pairs hit by the lanes that continue a row (per half warp;
-    // 4-bit counters, a saturated one only skews the heuristic)
-    uint64_t xo = act && !sw ? 1ull << (4 * xkey(entry_col<KIND>(rowc, ci[p]))) : 0ull;
-    for (int o = 8; o > 0; o >>= 1) xo += __shfl_xor_sync(0xffffffffu, xo, o);
-    uint64_t ao = 0;
+  for (int stp = 0; stp < kmax; ++stp) {
+    const bool sw = stp < total && rem == 0;
     const unsigned swm = __ballot_sync(0xffffffffu, sw);
+    uint64_t ao = 0;  // accumulator loads of this step (per half)
     for (unsigned qm = (swm | (swm >> 16)) & 0xffffu; qm; qm &= qm - 1) {
       const int q = __ffs(qm) - 1;
       const bool me = sw && (lane & 15) == q;
-      uint64_t add_x = 0, add_a = 0;
+      uint64_t add_a = 0;
       if (me) {
         int best = INT_MAX, pick = 0;
         for (unsigned m = left; m; m &= m - 1) {
           const int j = __ffs(m) - 1;
           const int ak = (lane ^ static_cast<int>((mw >> (4 * j)) & 15u)) & 15;
-          const int cost = 2 * static_cast<int>((ao >> (4 * ak)) & 15u) +
-                           static_cast<int>((xo >> (4 * ((fk >> (4 * j)) & 15u))) & 15u);
+          const int64_t r = row_of(j);
+          int cost = occ_get(ao, ak) + occ_get(sc.st[h][stp + nr[j]], ak);
+          for (int e = 0; e < nr[j]; ++e)
+            cost += occ_get(sc.x[h][stp + e], xkey(entry_col<KIND>(r, ci[src[j] + e])));
           if (cost < best) {
             best = cost;
             pick = j;
@@ -172,20 +182,19 @@ __device__ void order_rows(const CI* __restrict__ ci, const int64_t (&src)[kRows
         cw |= static_cast<uint64_t>(nr[pick]) << (4 * k);
         ++k;
         rem = nr[pick];
-        p = src[pick];
-        rowc = row_of(pick);
-        add_x = 1ull << (4 * ((fk >> (4 * pick)) & 15u));
-        add_a = 1ull << (4 * ((lane ^ static_cast<int>((mw >> (4 * pick)) & 15u)) & 15));
+        const int ak = (lane ^ static_cast<int>((mw >> (4 * pick)) & 15u)) & 15;
+        const int64_t r = row_of(pick);
+        for (int e = 0; e < nr[pick]; ++e)
+          sc.x[h][stp + e] = occ_add(sc.x[h][stp + e], xkey(entry_col<KIND>(r, ci[src[pick] + e])));
+        sc.st[h][stp + nr[pick]] = occ_add(sc.st[h][stp + nr[pick]], ak);
+        add_a = 1ull << (4 * ak);
       }
-      const int from = (lane & 16) | q;
-      xo += __shfl_sync(0xffffffffu, add_x, from);
-      ao += __shfl_sync(0xffffffffu, add_a, from);
+      ao += __shfl_sync(0xffffffffu, add_a, (lane & 16) | q);
+      __syncwarp();
     }
-    if (act) {
-      --rem;
-      ++p;
-    }
+    if (stp < total) --rem;
   }
+  __syncwarp();
 }
 
 struct TileGeom {
@@ -289,6 +298,7 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
     uint64_t* __restrict__ counts, uint64_t* __restrict__ order, uint64_t* __restrict__ masks,
     IT* __restrict__ t_inner,
     VB* __restrict__ t_values, int64_t* __restrict__ ovf_rows) {
+  __shared__ OrderScratch scratch[4];  // one per warp (128 threads)
   const int lane = threadIdx.x & 31;
   const unsigned below = (1u << lane) - 1u;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(128) tiles_fill_kernel(
       const int kmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(total)));
       uint64_t ow, cw;
       order_rows<KIND, CI, VB>(ci, src, nr, mw, geo.rs + kGroupRows * g, geo.col0 + t * geo.T, total,
-                               kmax, ow, cw);
+                               kmax, scratch[threadIdx.x >> 5], ow, cw);
       counts[(cnt_ptr[g] + k) * 32 + lane] = cw;
       order[(cnt_ptr[g] + k) * 32 + lane] = ow;
       if (lane == 0) masks[cnt_ptr[g] + k] = mw;
