@@ -337,6 +337,22 @@ int dacsr_spmv_dev_alpha(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int3
                          const double* alpha_dev, double beta, int64_t row_start, int64_t row_end,
                          void* stream);
 
+/* dacsr_spmv_dev_alpha on the TILED kernel that also returns ||y||^2 by
+ * 512-row groups: group_sumsq[r / 512] = the sum of y[r]^2 (y as stored)
+ * over the group's rows in the fixed group tree of dacsr_sumsq_chunks — the
+ * power iteration's norm without a second pass over y.  Needs whole groups:
+ * the layout's row_start, row_start and row_end (unless the layout's end)
+ * multiples of 512, no rows left out of the layout, the naive order;
+ * DACSR_ERR_PLAN / DACSR_ERR_VARIANT otherwise (run dacsr_sumsq_chunks
+ * then).  dacsr_sumsq_from_groups folds the group sums into chunk partials
+ * (chunk a multiple of 512) identical to dacsr_sumsq_chunks'. */
+int dacsr_spmv_dev_alpha_sumsq(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t variant,
+                               int32_t order, const void* x, int64_t x_offset, void* y,
+                               const double* alpha_dev, double beta, int64_t row_start,
+                               int64_t row_end, double* group_sumsq_dev, void* stream);
+int dacsr_sumsq_from_groups(const double* group_sumsq_dev, int64_t n, int64_t chunk,
+                            double* partial_dev, void* stream);
+
 /* spmv with HOST x / y, copies overlapped with the kernels: rows split into
  * the row ranges of plans[0..npieces) (ascending, covering the rows); piece
  * p needs x[0, min(ncols, row_end_p + w)) with w the bandwidth (max |col -

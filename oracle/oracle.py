@@ -306,27 +306,31 @@ def gen_normal(seed, i0, i1, table):
 # ---- deterministic norm restatement (csrc/aux.cu sumsq_kernel) -----------
 
 def sumsq_chunks(y, chunk):
-    """Per-chunk sum of y^2 in the device kernel's fixed order: 256 lanes
-    each fold y[c0+t::256] left to right, a 5-step xor butterfly per 32
-    lanes, then the 8 warp sums left to right."""
+    """Per-chunk sum of y^2 in the device's fixed GROUP TREE (csrc/aux.cu
+    group_sumsq, also the TILED kernel's fused epilogue): a chunk is cut into
+    groups of 512 values from its start; in a group lane l folds
+    sq(y[32j + l]), j = 0..15 in order (values past the end are skipped:
+    adding +0.0 to a sum that started at +0.0 changes nothing), a 5-step xor
+    butterfly over the 32 lanes gives the group sum, and the chunk's partial
+    is its group sums folded left to right."""
     y = np.asarray(y, dtype=np.float64)
     n = len(y)
     out = []
+    lanes = np.arange(32)
     for c0 in range(0, n, chunk):
         seg = y[c0:min(n, c0 + chunk)]
-        lanes = np.zeros(256)
-        for t in range(256):
-            acc = 0.0
-            for v in seg[t::256].tolist():
-                acc = acc + v * v
-            lanes[t] = acc
-        w = lanes.reshape(8, 32).copy()
+        ng = (len(seg) + 511) // 512
+        pad = np.zeros(ng * 512)
+        pad[:len(seg)] = seg
+        sq = (pad * pad).reshape(ng, 16, 32)
+        acc = np.zeros((ng, 32))
+        for j in range(16):
+            acc = acc + sq[:, j, :]
         for o in (16, 8, 4, 2, 1):
-            idx = np.arange(32) ^ o
-            w = w + w[:, idx]
+            acc = acc + acc[:, lanes ^ o]
         t = 0.0
-        for k in range(8):
-            t = t + float(w[k, 0])
+        for v in acc[:, 0].tolist():
+            t = t + v
         out.append(t)
     return np.array(out)
 

@@ -136,12 +136,15 @@ _SIGNATURES = {
                    ctypes.c_int),
     "dacsr_spmv_dev_alpha": ([_P(Matrix), _P(Plan), _i32, _i32, _vp, _i64, _vp, _vp, _d, _i64,
                               _i64, _vp], ctypes.c_int),
+    "dacsr_spmv_dev_alpha_sumsq": ([_P(Matrix), _P(Plan), _i32, _i32, _vp, _i64, _vp, _vp, _d,
+                                    _i64, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_scale": ([_vp, _i32, _i64, _d, _vp], ctypes.c_int),
     "dacsr_norm_alpha": ([_vp, _i64, _vp, _vp, _vp], ctypes.c_int),
     "dacsr_scale_dev": ([_vp, _i32, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_spmv_host_streamed": ([_P(Matrix), _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _d, _d,
                                   _i64, _vp, _vp, _vp], ctypes.c_int),
     "dacsr_sumsq_chunks": ([_vp, _i32, _i64, _i64, _vp, _vp], ctypes.c_int),
+    "dacsr_sumsq_from_groups": ([_vp, _i64, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_sum_ordered": ([_vp, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_bandwidth": ([_P(Matrix), _vp, _vp], ctypes.c_int),
     "dacsr_csr_to_da": ([_P(Matrix), _vp, _i32, _vp], ctypes.c_int),

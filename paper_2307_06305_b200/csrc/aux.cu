@@ -125,26 +125,61 @@ __global__ void scale_kernel(VT* y, int64_t n, double beta) {
   }
 }
 
-// one CTA per chunk; fixed strided assignment + fixed tree => deterministic
+// Deterministic ||y||^2 — the fixed GROUP TREE (also produced by the TILED
+// SpMV's epilogue, tiled.cuh): a chunk is cut into groups of 512 values from
+// its start; in a group lane l folds sq(y[32j + l]), j = 0..15 in order
+// (values past the end are skipped), then a 5-step xor butterfly over the 32
+// lanes gives the group sum; the chunk's partial is its group sums folded
+// left to right.  One CTA per chunk, a group per warp and round.
+template <class VT>
+__device__ __forceinline__ double group_sumsq(const VT* y, int64_t g0, int64_t end, int lane) {
+  double acc = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < 16; ++j) {
+    const int64_t i = g0 + 32 * j + lane;
+    if (i < end) {
+      const double v = to_f64(y[i]);
+      acc = __dadd_rn(acc, __dmul_rn(v, v));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  return acc;
+}
+
 template <class VT>
 __global__ void __launch_bounds__(256) sumsq_kernel(const VT* y, int64_t n, int64_t chunk,
                                                     double* partial) {
   __shared__ double red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t c1 = min(n, c0 + chunk);
-  double acc = 0.0;
-  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-    const double v = to_f64(y[i]);
-    acc = __dadd_rn(acc, __dmul_rn(v, v));
+  double t = 0.0;
+  for (int64_t base = c0; base < c1; base += 8 * 512) {
+    const int64_t g0 = base + 512 * warp;
+    const double acc = g0 < c1 ? group_sumsq(y, g0, c1, lane) : 0.0;
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 0; w < 8; ++w)
+        if (base + 512 * w < c1) t = __dadd_rn(t, red[w]);
+    __syncthreads();
   }
-  for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < (blockDim.x >> 5); ++w) t = __dadd_rn(t, red[w]);
-    partial[blockIdx.x] = t;
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// chunk partials from group sums already in memory (the fused epilogue's):
+// partial[c] = the chunk's groups folded left to right
+__global__ void chunks_from_groups_kernel(const double* __restrict__ gsq, int64_t ngroups,
+                                          int64_t gpc, int64_t nchunks,
+                                          double* __restrict__ partial) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  double t = 0.0;
+  for (int64_t k = 0; k < gpc; ++k) {
+    const int64_t g = c * gpc + k;
+    if (g < ngroups) t = __dadd_rn(t, gsq[g]);
   }
+  partial[c] = t;
 }
 
 __global__ void sum_ordered_kernel(const double* p, int64_t m, double* out) {
@@ -376,6 +411,18 @@ int dacsr_sumsq_chunks(const void* y, int32_t vdt, int64_t n, int64_t chunk, dou
   else if (vdt == DACSR_F32) sumsq_kernel<float><<<static_cast<unsigned>(m), 256, 0, st>>>(static_cast<const float*>(y), n, chunk, partial);
   else return DACSR_ERR_DTYPE;
   return check_launch("sumsq_kernel");
+}
+
+int dacsr_sumsq_from_groups(const double* group_sumsq, int64_t n, int64_t chunk, double* partial,
+                            void* stream) {
+  if (n < 0 || chunk <= 0 || (chunk & 511) || (n > 0 && (!group_sumsq || !partial)))
+    return DACSR_ERR_ARG;
+  if (n == 0) return DACSR_OK;
+  const int64_t ngroups = (n + 511) / 512, gpc = chunk / 512, m = (n + chunk - 1) / chunk;
+  chunks_from_groups_kernel<<<static_cast<unsigned>((m + 127) / 128), 128, 0,
+                              static_cast<cudaStream_t>(stream)>>>(group_sumsq, ngroups, gpc, m,
+                                                                   partial);
+  return check_launch("chunks_from_groups_kernel");
 }
 
 int dacsr_norm_alpha(const double* partial, int64_t m, double* norm_out, double* alpha_out,

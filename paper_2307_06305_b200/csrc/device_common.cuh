@@ -121,6 +121,15 @@ __device__ __forceinline__ void epilogue(VT* y, int64_t r, double acc, double al
   if (beta != 0.0) out = __dadd_rn(out, __dmul_rn(beta, to_f64(y[r])));
   store_rounded(y + r, out);
 }
+// the same, returning y[r] as stored (rounded to VT) for a fused ||y||^2
+template <class VT>
+__device__ __forceinline__ double epilogue_stored(VT* y, int64_t r, double acc, double alpha,
+                                                  double beta) {
+  double out = __dmul_rn(alpha, acc);
+  if (beta != 0.0) out = __dadd_rn(out, __dmul_rn(beta, to_f64(y[r])));
+  store_rounded(y + r, out);
+  return to_f64(y[r]);
+}
 
 // Exact thread-sequential sums in the reference's three orders
 // (_numba_kernels.py:82-91 naive, :110-132 multi_acc3, :135-160 strip_mined4).

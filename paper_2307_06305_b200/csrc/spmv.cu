@@ -179,6 +179,28 @@ int dacsr_spmv_dev_alpha(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int3
   }
 }
 
+int dacsr_spmv_dev_alpha_sumsq(const dacsr_matrix_t* a, const dacsr_plan_t* plan, int32_t variant,
+                               int32_t order, const void* x, int64_t x_offset, void* y,
+                               const double* alpha_dev, double beta, int64_t row_start,
+                               int64_t row_end, double* group_sumsq, void* stream) {
+  if (!a || !y || !alpha_dev || !group_sumsq || row_start < 0 || row_end < row_start ||
+      row_end > a->nrows)
+    return DACSR_ERR_ARG;
+  if (row_end == row_start) return DACSR_OK;
+  if (!a->rowptr || (a->nnz > 0 && (!a->colids || !a->values || !x))) return DACSR_ERR_ARG;
+  if (variant != DACSR_VARIANT_TILED) return DACSR_ERR_VARIANT;
+  if (order < DACSR_ORDER_NAIVE || order > DACSR_ORDER_TREE) return DACSR_ERR_VARIANT;
+  Req q{plan, variant, order, x, x_offset, y, 0.0, beta, row_start, row_end,
+        static_cast<cudaStream_t>(stream), alpha_dev, group_sumsq};
+  switch (a->values_dtype) {
+    case DACSR_F64: return launch_values_f64(a, q);
+    case DACSR_F32: return launch_values_f32(a, q);
+    case DACSR_F16: return launch_values_f16(a, q);
+    case DACSR_BF16: return launch_values_bf16(a, q);
+    default: return DACSR_ERR_DTYPE;
+  }
+}
+
 // Host-buffer SpMV with the copies overlapped (see hostpath.py): rows are
 // split into the plans' row ranges; piece p needs x[0, min(ncols, r1_p + w))
 // (w = bandwidth).  h2d: the x prefix not yet sent; comp: waits for it, runs

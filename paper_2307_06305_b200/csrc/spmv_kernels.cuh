@@ -57,6 +57,9 @@ struct Scal {
   // alpha read from device memory at the epilogue (power iteration: the
   // previous norm's 1/s, computed on the device); nullptr: `alpha`
   const double* alpha_dev = nullptr;
+  // TILED only: sum of y^2 of every 512-row group in the fixed group tree
+  // (aux.cu group_sumsq), stored at group_sumsq[row / 512]; nullptr: off
+  double* group_sumsq = nullptr;
   __device__ __forceinline__ double a() const { return alpha_dev ? __ldg(alpha_dev) : alpha; }
 };
 
@@ -1079,6 +1082,7 @@ struct Req {
   int64_t rs, re;
   cudaStream_t stream;
   const double* alpha_dev = nullptr;
+  double* group_sumsq = nullptr;
 };
 
 // per-value-type launchers (one translation unit each)
@@ -1194,7 +1198,9 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
   if (rows <= 0) return DACSR_OK;
   const int order = q.order;
   const bool exact = order != DACSR_ORDER_TREE;
-  Scal s{q.alpha, q.beta, order, 0, q.alpha_dev};
+  Scal s{q.alpha, q.beta, order, 0, q.alpha_dev, q.group_sumsq};
+  // the fused group sums exist in the TILED epilogue only
+  if (q.group_sumsq && q.variant != DACSR_VARIANT_TILED) return DACSR_ERR_VARIANT;
   const int sms = sm_count();
   const bool can_bulk = aligned16(a->values) && aligned16(a->colids);
 
@@ -1386,6 +1392,13 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
           (td->ngroups > 0 && (!td->ent_ptr || !td->cnt_ptr || !td->tile_lo || !td->skip)) ||
           (td->nblocks > 0 && (!td->counts || !td->order || !td->masks)) || (td->total > 0 && (!td->inner || !td->values)) ||
           (td->n_ovf > 0 && !td->ovf_rows) || (a->nnz > 0 && (!a->colids || !a->values)))
+        return DACSR_ERR_PLAN;
+      // fused group sums: whole 512-row groups of y (y index 0 on a group
+      // boundary), no rows left to the warp-per-row pass
+      if (q.group_sumsq &&
+          ((td->row_start & 511) || ((q.rs - td->row_start) & 511) ||
+           (q.re != td->row_end && ((q.re - td->row_start) & 511)) || td->n_ovf > 0 ||
+           order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4))
         return DACSR_ERR_PLAN;
       if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) {
         // the tiled fold specialises the naive order; the others run row blocks

@@ -26,7 +26,10 @@
 // 15 consumer warps + the producer = 16 warps, 4 per SM sub-partition: the
 // register file is split per sub-partition, so a 17th warp would cap every
 // thread at 96 registers (measured: spills) instead of 128
-constexpr int kTileWarps = 15;  // consumer warps (groups) per CTA
+#ifndef DACSR_TILED_WARPS
+#define DACSR_TILED_WARPS 15
+#endif
+constexpr int kTileWarps = DACSR_TILED_WARPS;  // consumer warps (groups) per CTA
 constexpr int kTileRows = 16;   // rows per lane
 #ifndef DACSR_TILED_G
 #define DACSR_TILED_G 2  // entries per lane per packed step (layout step_group)
@@ -552,11 +555,28 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
     // the chunk's rows: y = alpha * sum (+ beta * y)
     if (has) {
       const unsigned sk = ldg(ta.skip + 32 * g + lane);
+      if (s.group_sumsq == nullptr) {
 #pragma unroll 4
-      for (int j = 0; j < kTileRows; ++j) {
-        const int64_t r = lrow + 32 * j;
-        if (r >= rs && r < re && !((sk >> j) & 1u))
-          epilogue(m.y, r, lds_f64(wa + 256u * j), s.a(), s.beta);
+        for (int j = 0; j < kTileRows; ++j) {
+          const int64_t r = lrow + 32 * j;
+          if (r >= rs && r < re && !((sk >> j) & 1u))
+            epilogue(m.y, r, lds_f64(wa + 256u * j), s.a(), s.beta);
+        }
+      } else {
+        // ... and the group's sum of y^2 in the fixed group tree: lane l
+        // folds its rows 32j + l in j order, then the xor butterfly
+        // (aux.cu group_sumsq restates it for a y already in memory)
+        double sq = 0.0;
+#pragma unroll 4
+        for (int j = 0; j < kTileRows; ++j) {
+          const int64_t r = lrow + 32 * j;
+          if (r >= rs && r < re) {
+            const double v = epilogue_stored(m.y, r, lds_f64(wa + 256u * j), s.a(), s.beta);
+            sq = __dadd_rn(sq, __dmul_rn(v, v));
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+        if (lane == 0) s.group_sumsq[(ta.row0 + 512 * g) >> 9] = sq;
       }
     }
     __syncwarp();

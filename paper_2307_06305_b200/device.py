@@ -93,6 +93,7 @@ class DeviceMatrix:
         self._launch_cache = {}
         self._spmv_fn = _native.lib().dacsr_spmv
         self._spmv_dev_alpha_fn = _native.lib().dacsr_spmv_dev_alpha
+        self._spmv_dev_alpha_sumsq_fn = _native.lib().dacsr_spmv_dev_alpha_sumsq
         self.tuned_kernel = None
         if plan:
             self.build_plan(cap=cap, long_len=long_len)
@@ -570,11 +571,14 @@ class DeviceMatrix:
 
     # ---- the multiply ---------------------------------------------------------
     def spmv_into(self, x, y, alpha=1.0, beta=0.0, variant="rowblock", order=0, x_offset=0,
-                  row_start=None, row_end=None, stream=None):
+                  row_start=None, row_end=None, stream=None, group_sumsq=None):
         """Launch y = alpha*A@x + beta*y on device tensors (no validation
         beyond the C ABI's; ``spmv`` is the validating entry point).
         ``alpha`` may be a one-element float64 CUDA tensor: the kernel reads it
         from device memory (dacsr_spmv_dev_alpha; no alpha == 0 short-cut).
+        ``group_sumsq`` (with a device alpha, TILED only; see
+        ``fused_sumsq_ok``): a float64 tensor that receives the sum of y^2 of
+        every 512-row group at index row // 512 (dacsr_spmv_dev_alpha_sumsq).
 
         The (variant, order, row range) -> (code, plan) resolution is cached
         per matrix, so a launch costs one ctypes call (a few microseconds of
@@ -594,7 +598,12 @@ class DeviceMatrix:
             sp = torch.cuda.current_stream(self.device).cuda_stream
         else:
             sp = stream.cuda_stream
-        if isinstance(alpha, torch.Tensor):  # alpha in device memory (one float64)
+        if group_sumsq is not None:
+            status = self._spmv_dev_alpha_sumsq_fn(desc, plan_ref, code, order_code,
+                                                   x.data_ptr() if x is not None else None,
+                                                   x_offset, y.data_ptr(), alpha.data_ptr(), beta,
+                                                   rs, re, group_sumsq.data_ptr(), sp)
+        elif isinstance(alpha, torch.Tensor):  # alpha in device memory (one float64)
             status = self._spmv_dev_alpha_fn(desc, plan_ref, code, order_code,
                                              x.data_ptr() if x is not None else None, x_offset,
                                              y.data_ptr(), alpha.data_ptr(), beta, rs, re, sp)
@@ -605,6 +614,21 @@ class DeviceMatrix:
         if status:
             _native.check(status, "dacsr_spmv")
         return y
+
+    def fused_sumsq_ok(self, variant, order=0, row_start=None, row_end=None):
+        """True if spmv_into(..., group_sumsq=...) can run for this variant
+        and row range: the TILED kernel in the naive order, its layout built
+        from a row that is a multiple of 512 with no rows left out, and the
+        range made of whole 512-row groups (dacsr_spmv_dev_alpha_sumsq)."""
+        if variant != "tiled" or order != _native.ORDER_NAIVE:
+            return False
+        if self._tiled is None:
+            self.build_tiles()
+        tl = self._tiled[1]
+        rs = self.row_start if row_start is None else int(row_start)
+        re = self.row_end if row_end is None else int(row_end)
+        return (tl.n_ovf == 0 and tl.row_start % 512 == 0 and (rs - tl.row_start) % 512 == 0
+                and (re == tl.row_end or (re - tl.row_start) % 512 == 0))
 
     def __repr__(self):
         return (f"DeviceMatrix({self.kind}, {self.nrows}x{self.ncols}, nnz={self.nnz}, "

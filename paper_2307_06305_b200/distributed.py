@@ -168,7 +168,12 @@ class CudaLocalOp:
         self.plan = plan
         self.chunk = chunk
         self.kind = kind
-        cut0, cut1 = min(b, n_local), max(min(b, n_local), n_local - b)
+        # interior rows need no halo; the cuts sit on 512-row group
+        # boundaries (a few rows that need no halo join the strips) so that
+        # every launch covers whole groups: the TILED epilogue then returns
+        # the groups' sums of y^2 (no second pass over y for the norm)
+        cut0 = min((b + 511) // 512 * 512, n_local)
+        cut1 = max(cut0, (n_local - b) // 512 * 512)
         self.ranges = [(cut0, cut1), (0, cut0), (cut1, n_local)]  # interior first
         name, order = resolve_variant(variant)
         self.order = order
@@ -194,19 +199,34 @@ class CudaLocalOp:
                             for dm in self.mats]
         # CSR local colids stay global: x index = col - lo
         self.x_offset = plan.x_offset if kind == "da" else -plan.lo
+        self.fused = bool(n_local) and chunk % 512 == 0 and all(
+            dm is None or dm.fused_sumsq_ok(k, self.order, r0, r1)
+            for dm, k, (r0, r1) in zip(self.mats, self.kernels, self.ranges))
+        self.group_sumsq = (torch.empty((n_local + 511) // 512, dtype=torch.float64,
+                                        device=rowptr.device) if self.fused else None)
 
     def spmv_part(self, which, x_ext, y, alpha, stream=None):
         dm = self.mats[which]
         if dm is not None:
             r0, r1 = self.ranges[which]
+            fused = self.fused and isinstance(alpha, torch.Tensor)
             dm.spmv_into(x_ext, y, alpha, 0.0, self.kernels[which], self.order,
-                         x_offset=self.x_offset, row_start=r0, row_end=r1, stream=stream)
+                         x_offset=self.x_offset, row_start=r0, row_end=r1, stream=stream,
+                         group_sumsq=self.group_sumsq if fused else None)
 
     device_norm = True  # the norm and the next alpha stay on the device
 
     def partials(self, y):
         from .power import chunk_partials
         return chunk_partials(y, self.chunk).clone()
+
+    def partials_after_spmv(self, y):
+        """The chunk partials of the y the three spmv_part launches just
+        wrote (device alpha): from their fused group sums when available."""
+        if not self.fused:
+            return self.partials(y)
+        from .power import partials_from_groups
+        return partials_from_groups(self.group_sumsq, self.n_local, self.chunk).clone()
 
     def fold(self, allp):
         from .power import fold_ordered
@@ -270,7 +290,8 @@ def power_iteration(op, plan, x0_own, iters, group=None, overlap=True, counts=No
         for k in range(iters):
             nxt = 1 - cur
             dist_spmv(op, bufs[cur], bufs[nxt][own], alpha, plan, group, overlap)
-            op.norm_alpha(gather_partials(op.partials(bufs[nxt][own]), group, counts),
+            after = getattr(op, "partials_after_spmv", op.partials)
+            op.norm_alpha(gather_partials(after(bufs[nxt][own]), group, counts),
                           norms[k + 1:k + 2], alpha)
             cur = nxt
         x = bufs[cur][own].clone()

@@ -1,8 +1,11 @@
 """Normalised power iteration x <- A x / ||A x||_2 (config C5) on one GPU.
 
 The norm is deterministic: ``dacsr_sumsq_chunks`` reduces y^2 over fixed
-row chunks with a fixed tree, ``dacsr_sum_ordered`` folds the chunk
-partials in index order.  With rank boundaries on chunk boundaries the
+row chunks with a fixed tree (512-row groups: 16 values per lane, an xor
+butterfly, the groups left to right), ``dacsr_sum_ordered`` folds the chunk
+partials in index order.  The TILED SpMV produces the same group sums in its
+epilogue (``spmv_into(group_sumsq=...)``), so an iteration does not read y a
+second time.  With rank boundaries on chunk boundaries the
 multi-GPU run (distributed.py) folds the very same partials, so 1/2/4/8
 GPUs produce bit-identical iterates.  The normalisation is folded into the
 next SpMV's alpha (y_k = (1/s_{k-1}) * A y_{k-1}), i.e. the reference API's
@@ -29,6 +32,19 @@ def chunk_partials(y, chunk=DEFAULT_CHUNK, stream=None, out=None):
     _native.check(_native.lib().dacsr_sumsq_chunks(
         ctypes.c_void_p(y.data_ptr()), _native.dtype_code(y.dtype), n, chunk,
         ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)), "dacsr_sumsq_chunks")
+    return out[:m]
+
+
+def partials_from_groups(group_sumsq, n, chunk=DEFAULT_CHUNK, stream=None, out=None):
+    """Per-chunk sums of y^2 from the 512-row group sums a fused SpMV stored
+    (DeviceMatrix.spmv_into(group_sumsq=...)): the very partials
+    ``chunk_partials`` computes from y, without reading y again."""
+    m = (n + chunk - 1) // chunk
+    if out is None:
+        out = torch.empty(max(m, 1), dtype=torch.float64, device=group_sumsq.device)
+    _native.check(_native.lib().dacsr_sumsq_from_groups(
+        ctypes.c_void_p(group_sumsq.data_ptr()), n, chunk, ctypes.c_void_p(out.data_ptr()),
+        _stream_ptr(stream)), "dacsr_sumsq_from_groups")
     return out[:m]
 
 
@@ -91,6 +107,12 @@ class PowerIteration:
         self.partials = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
         self.alpha = torch.empty(1, dtype=torch.float64, device=dev)
         self.norms = torch.empty(iters + 1, dtype=torch.float64, device=dev)
+        # ||y||^2 out of the SpMV's own epilogue where the kernel offers it
+        # (TILED, whole 512-row groups): no second pass over y
+        self.fused = (chunk % 512 == 0 and dm.nrows == x0.numel()
+                      and dm.fused_sumsq_ok(variant, order))
+        self.group_sumsq = (torch.empty((x0.numel() + 511) // 512, dtype=torch.float64, device=dev)
+                            if self.fused else None)
         self.graph = None
         if graph:
             self._launch()  # warm: derived layout, launch-config caches
@@ -110,9 +132,13 @@ class PowerIteration:
         cur = 0
         for k in range(self.iters):
             dm.spmv_into(self.bufs[cur], self.bufs[1 - cur], self.alpha, 0.0, self.variant,
-                         self.order, stream=stream)
+                         self.order, stream=stream, group_sumsq=self.group_sumsq)
             cur = 1 - cur
-            chunk_partials(self.bufs[cur], chunk, stream, out=self.partials)
+            if self.fused:
+                partials_from_groups(self.group_sumsq, self.x0.numel(), chunk, stream,
+                                     out=self.partials)
+            else:
+                chunk_partials(self.bufs[cur], chunk, stream, out=self.partials)
             norm_alpha(self.partials, self.norms[k + 1:k + 2], self.alpha, stream)
         self.cur = cur
 

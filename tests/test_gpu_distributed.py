@@ -176,3 +176,37 @@ def test_power_iteration_graph_replay_matches_eager(cuda):
         x_g, n_g = pi.result()
         assert n_g == n_e
         assert torch.equal(x_g.view(torch.int64), x_e.view(torch.int64))
+
+
+def test_fused_norm_in_the_power_iteration(cuda):
+    """On the TILED kernel the power iteration takes ||y||^2 from the SpMV's
+    epilogue (512-row group sums); the norms and the iterate equal the
+    separate-pass run's, and the three-launch rank-local operator returns the
+    same chunk partials."""
+    from paper_2307_06305_b200.power import PowerIteration
+    n, b = 1 << 17, 20000
+    arr = banded_arrays(n, b, 5.0, 12, SEED, cuda)  # <= 12 entries per row: none left out
+    dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"])
+    x0 = normal_vector(n, 11, cuda)
+    fused = PowerIteration(dm, x0, iters=6, chunk=4096, variant="tiled")
+    assert fused.fused
+    fused.run()
+    xf, nf = fused.result()
+    plain = PowerIteration(dm, x0, iters=6, chunk=4096, variant="tiled")
+    plain.fused, plain.group_sumsq = False, None
+    plain.run()
+    xp, npl = plain.result()
+    assert nf == npl and torch.equal(xf.view(torch.int64), xp.view(torch.int64))
+    # one rank's operator: interior + two strips, cuts on group boundaries
+    part = D.RowPartition.equal(n, 1, align=4096)
+    plan = D.halo_plan(part, 0, b)
+    op = D.CudaLocalOp("da", arr["rowptr"], arr["offsets"], arr["values"], n, plan, 4096, b)
+    assert op.fused and all(r0 % 512 == 0 and r1 % 512 == 0 for r0, r1 in op.ranges)
+    alpha = torch.tensor([0.5], dtype=torch.float64, device=cuda)
+    x_ext = x0[plan.lo:plan.hi].clone()
+    y = torch.empty(n, dtype=torch.float64, device=cuda)
+    for which in range(3):
+        op.spmv_part(which, x_ext, y, alpha)
+    got = op.partials_after_spmv(y).cpu().numpy()
+    want = op.partials(y).cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

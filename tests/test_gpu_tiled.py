@@ -173,3 +173,48 @@ def test_skewed_rows_and_default_selection(cuda):
     assert dm.stats.scatter < 0.5
     from paper_2307_06305_b200.spmv import kernel_for
     assert kernel_for(dm, "exact", 0) == "sliced_pipe"
+
+
+def test_fused_group_sumsq(cuda):
+    """spmv_into(group_sumsq=...) stores the sums of y^2 of whole 512-row
+    groups in the fixed group tree: the chunk partials folded from them are
+    the bits dacsr_sumsq_chunks computes from y (and the oracle restates);
+    row ranges made of whole groups write only their groups; anything else
+    is refused."""
+    from paper_2307_06305_b200.errors import DeviceError
+    from paper_2307_06305_b200.power import chunk_partials, partials_from_groups
+    n = (1 << 15) + 777  # the last group is partial
+    arr = banded_arrays(n, 2000, 5.0, 12, 6, cuda, kinds=("da",))  # <= 12 entries per row
+    dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"])
+    dm.build_tiles()
+    assert dm.tiles_info()["n_ovf"] == 0 and dm.fused_sumsq_ok("tiled")
+    x = normal_vector(n, 9, cuda)
+    alpha = torch.tensor([0.37], dtype=torch.float64, device=cuda)
+    ng = (n + 511) // 512
+    gs = torch.full((ng,), float("nan"), dtype=torch.float64, device=cuda)
+    y = torch.empty(n, dtype=torch.float64, device=cuda)
+    dm.spmv_into(x, y, alpha, 0.0, "tiled", 0, group_sumsq=gs)
+    y2 = dm.spmv_into(x, torch.empty_like(y), alpha, 0.0, "tiled", 0)
+    assert torch.equal(y.view(torch.int64), y2.view(torch.int64))
+    for chunk in (512, 4096, 1 << 16):
+        fused = partials_from_groups(gs, n, chunk).cpu().numpy()
+        direct = chunk_partials(y, chunk).cpu().numpy()
+        assert np.array_equal(fused.view(np.uint64), direct.view(np.uint64)), chunk
+        want = oracle.sumsq_chunks(y.cpu().numpy(), chunk)
+        assert np.array_equal(fused.view(np.uint64), want.view(np.uint64)), chunk
+    # beta != 0 and a range of whole groups: only its groups are written
+    gs2 = torch.full((ng,), -1.0, dtype=torch.float64, device=cuda)
+    y3 = y.clone()
+    dm.spmv_into(x, y3, alpha, 0.5, "tiled", 0, row_start=1024, row_end=8192, group_sumsq=gs2)
+    g2 = gs2.cpu().numpy()
+    assert (g2[:2] == -1.0).all() and (g2[16:] == -1.0).all()
+    want = oracle.sumsq_chunks(y3.cpu().numpy()[1024:8192], 512)
+    assert np.array_equal(g2[2:16].view(np.uint64), want.view(np.uint64))
+    assert dm.fused_sumsq_ok("tiled", 0, 1024, 8192)
+    # ranges that cut a group, other kernels
+    assert not dm.fused_sumsq_ok("tiled", 0, 100, 8192)
+    with pytest.raises(DeviceError):
+        dm.spmv_into(x, y3, alpha, 0.0, "tiled", 0, row_start=100, row_end=8192, group_sumsq=gs2)
+    assert not dm.fused_sumsq_ok("sliced_pipe")
+    with pytest.raises(DeviceError):
+        dm.spmv_into(x, y3, alpha, 0.0, "sliced_pipe", 0, group_sumsq=gs2)
