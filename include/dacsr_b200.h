@@ -360,12 +360,14 @@ int dacsr_sumsq_from_groups(const double* group_sumsq_dev, int64_t n, int64_t ch
  * values; s_h2d carries the x copies, s_comp the kernels.  If y_host is
  * page-locked and mapped (cudaHostAlloc / cudaHostRegister under UVA) the
  * kernels store y straight into it over PCIe and y_dev / s_d2h are unused;
- * otherwise y returns through y_dev with D2H copies on s_d2h.  Blocks until
- * y_host is complete. */
+ * otherwise (or with y_through_device != 0: the copy engine moves large
+ * pieces a few per cent faster than the kernels' stores over the link) y
+ * returns through y_dev with D2H copies on s_d2h.  Blocks until y_host is
+ * complete. */
 int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans, int32_t npieces,
                              int32_t variant, int32_t order, const void* x_host, void* y_host,
                              void* x_dev, void* y_dev, double alpha, double beta, int64_t w,
-                             void* s_h2d, void* s_comp, void* s_d2h);
+                             void* s_h2d, void* s_comp, void* s_d2h, int32_t y_through_device);
 
 /* The reference's alpha == 0 short-cut (spmv/__init__.py:150-156):
  * y = 0 if beta == 0, y = (T)((double)beta * y) if beta not in {0, 1}. */

@@ -142,7 +142,7 @@ _SIGNATURES = {
     "dacsr_norm_alpha": ([_vp, _i64, _vp, _vp, _vp], ctypes.c_int),
     "dacsr_scale_dev": ([_vp, _i32, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_spmv_host_streamed": ([_P(Matrix), _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _d, _d,
-                                  _i64, _vp, _vp, _vp], ctypes.c_int),
+                                  _i64, _vp, _vp, _vp, _i32], ctypes.c_int),
     "dacsr_sumsq_chunks": ([_vp, _i32, _i64, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_sumsq_from_groups": ([_vp, _i64, _i64, _vp, _vp], ctypes.c_int),
     "dacsr_sum_ordered": ([_vp, _i64, _vp, _vp], ctypes.c_int),

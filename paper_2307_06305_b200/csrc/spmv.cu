@@ -213,7 +213,7 @@ int dacsr_spmv_dev_alpha_sumsq(const dacsr_matrix_t* a, const dacsr_plan_t* plan
 int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans, int32_t npieces,
                              int32_t variant, int32_t order, const void* x_host, void* y_host,
                              void* x_dev, void* y_dev, double alpha, double beta, int64_t w,
-                             void* s_h2d, void* s_comp, void* s_d2h) {
+                             void* s_h2d, void* s_comp, void* s_d2h, int32_t y_through_device) {
   if (!a || !plans || npieces <= 0 || npieces > 64 || !x_host || !y_host || !x_dev || !y_dev ||
       w < 0)
     return DACSR_ERR_ARG;
@@ -231,6 +231,7 @@ int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans,
       y_mapped = pa.devicePointer;
     else
       cudaGetLastError();  // pageable memory: not an error, take the copy path
+    if (y_through_device) y_mapped = nullptr;
   }
   cudaEvent_t ev[128];
   int nev = 0;

@@ -24,13 +24,20 @@ from .spmv import kernel_for
 class StreamedHost:
     """Per-DeviceMatrix resources of the streamed host path (cached)."""
 
-    def __init__(self, dm, pieces=4, cuts=None):
-        # pieces: equal row pieces (C2: 1 -> 0.72 ms, 4 -> 0.61 ms, 16 -> 0.93 ms);
+    def __init__(self, dm, pieces=None, cuts=None, y_through_device=None):
+        # pieces: equal row pieces (C2: 1 -> 0.72 ms, 4 -> 0.61 ms, 16 -> 0.93 ms;
+        # C3, 134 MB of x and of y: 4 -> 3.77 ms, 8 -> 3.55 ms with y returned by
+        # the copy engine, 3.72 ms with the kernels storing it over the link,
+        # 16 -> 3.62 / 4.06 ms: tools/e2e_c3_pieces.py);
         # cuts: interior cut points as row fractions instead (small first and
         # last pieces shorten the pipeline fill and drain)
         from .device import DeviceMatrix, bandwidth_device
         self.dm = dm
         n = dm.nrows
+        big = (dm.row_end - dm.row_start) * dm.values.element_size() >= (64 << 20)
+        if pieces is None:
+            pieces = 8 if big else 4
+        self.y_through_device = int(big if y_through_device is None else y_through_device)
         self.w = bandwidth_device(dm) if dm.nnz else 0
         if cuts is None:
             cuts = np.linspace(dm.row_start, dm.row_end, pieces + 1).astype(np.int64)
@@ -94,7 +101,8 @@ class StreamedHost:
             ctypes.byref(dm.desc), plans, len(self.views), code, int(order),
             x_host.ctypes.data, y_host.ctypes.data, self.x.data_ptr(), self.y.data_ptr(),
             float(alpha), float(beta), int(self.w), self.s_h2d.cuda_stream,
-            self.s_comp.cuda_stream, self.s_d2h.cuda_stream), "dacsr_spmv_host_streamed")
+            self.s_comp.cuda_stream, self.s_d2h.cuda_stream, self.y_through_device),
+            "dacsr_spmv_host_streamed")
         return y_host
 
 
