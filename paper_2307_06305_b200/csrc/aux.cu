@@ -182,10 +182,26 @@ __global__ void chunks_from_groups_kernel(const double* __restrict__ gsq, int64_
   partial[c] = t;
 }
 
-__global__ void sum_ordered_kernel(const double* p, int64_t m, double* out) {
+// p[0] + p[1] + ... in index order, by one warp: 32 partials per coalesced
+// load (the next 32 in flight), folded left to right through shuffles — the
+// same sum, bit for bit, as one thread walking the array (which waits out a
+// memory latency every few elements: 0.10 ms for C5's 4096 partials)
+__device__ __forceinline__ double ordered_fold_warp(const double* __restrict__ p, int64_t m) {
+  const int lane = threadIdx.x & 31;
   double t = 0.0;
-  for (int64_t i = 0; i < m; ++i) t = __dadd_rn(t, p[i]);
-  *out = t;
+  double nxt = lane < m ? p[lane] : 0.0;
+  for (int64_t i = 0; i < m; i += 32) {
+    const double v = nxt;
+    nxt = i + 32 + lane < m ? p[i + 32 + lane] : 0.0;
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(32), m - i));
+    for (int k = 0; k < cnt; ++k) t = __dadd_rn(t, __shfl_sync(0xffffffffu, v, k));
+  }
+  return t;
+}
+
+__global__ void sum_ordered_kernel(const double* p, int64_t m, double* out) {
+  const double t = ordered_fold_warp(p, m);
+  if (threadIdx.x == 0) *out = t;
 }
 
 // the power iteration's norm on the device: s = sqrt(ordered fold of the
@@ -193,8 +209,8 @@ __global__ void sum_ordered_kernel(const double* p, int64_t m, double* out) {
 // operations as Python's math.sqrt and 1.0 / s
 __global__ void norm_alpha_kernel(const double* p, int64_t m, double* norm_out,
                                   double* alpha_out) {
-  double t = 0.0;
-  for (int64_t i = 0; i < m; ++i) t = __dadd_rn(t, p[i]);
+  const double t = ordered_fold_warp(p, m);
+  if (threadIdx.x != 0) return;
   const double sq = __dsqrt_rn(t);
   if (norm_out) *norm_out = sq;
   *alpha_out = __ddiv_rn(1.0, sq);
@@ -428,7 +444,7 @@ int dacsr_sumsq_from_groups(const double* group_sumsq, int64_t n, int64_t chunk,
 int dacsr_norm_alpha(const double* partial, int64_t m, double* norm_out, double* alpha_out,
                      void* stream) {
   if (!partial || m < 0 || !alpha_out) return DACSR_ERR_ARG;
-  norm_alpha_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(partial, m, norm_out,
+  norm_alpha_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(partial, m, norm_out,
                                                                      alpha_out);
   return check_launch("norm_alpha_kernel");
 }
@@ -448,7 +464,7 @@ int dacsr_scale_dev(void* y, int32_t vdt, int64_t n, const double* beta_dev, voi
 
 int dacsr_sum_ordered(const double* partial, int64_t m, double* out, void* stream) {
   if (!out || m < 0 || (m > 0 && !partial)) return DACSR_ERR_ARG;
-  sum_ordered_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(partial, m, out);
+  sum_ordered_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(partial, m, out);
   return check_launch("sum_ordered_kernel");
 }
 

@@ -113,6 +113,20 @@ __device__ __forceinline__ void store_rounded(__nv_bfloat16* p, double v) {
   *p = __double2bfloat16(v);
 }
 
+// the value store_rounded leaves in memory, widened back (no reload)
+template <class VT>
+__device__ __forceinline__ double as_stored(double v);
+template <> __device__ __forceinline__ double as_stored<double>(double v) { return v; }
+template <> __device__ __forceinline__ double as_stored<float>(double v) {
+  return static_cast<double>(__double2float_rn(v));
+}
+template <> __device__ __forceinline__ double as_stored<__half>(double v) {
+  return static_cast<double>(__half2float(__double2half(v)));
+}
+template <> __device__ __forceinline__ double as_stored<__nv_bfloat16>(double v) {
+  return static_cast<double>(__bfloat162float(__double2bfloat16(v)));
+}
+
 // y[r] = alpha*acc (+ beta*y[r] iff beta != 0); y is not read when beta == 0.
 template <class VT>
 __device__ __forceinline__ void epilogue(VT* y, int64_t r, double acc, double alpha,
@@ -128,7 +142,7 @@ __device__ __forceinline__ double epilogue_stored(VT* y, int64_t r, double acc, 
   double out = __dmul_rn(alpha, acc);
   if (beta != 0.0) out = __dadd_rn(out, __dmul_rn(beta, to_f64(y[r])));
   store_rounded(y + r, out);
-  return to_f64(y[r]);
+  return as_stored<VT>(out);
 }
 
 // Exact thread-sequential sums in the reference's three orders

@@ -14,7 +14,7 @@ import torch
 from paper_2307_06305_b200 import distributed as D
 from paper_2307_06305_b200.device import DeviceMatrix
 from paper_2307_06305_b200.gen import banded_arrays, normal_vector
-from paper_2307_06305_b200.power import chunk_partials, fold_ordered
+from paper_2307_06305_b200.power import chunk_partials, fold_ordered, partials_from_groups
 from paper_2307_06305_b200.workloads import BANDED_CONFIGS
 
 dev = torch.device("cuda")
@@ -46,6 +46,11 @@ out["spmv_interior_ms"] = timed(lambda: dm.spmv_into(x, y, 1.0, 0.0, "tiled", ro
                                                      row_end=cut1))
 out["spmv_strip_ms"] = timed(lambda: dm.spmv_into(x, y, 1.0, 0.0, "tiled", row_start=0,
                                                   row_end=cut0))
+alpha = torch.ones(1, dtype=torch.float64, device=dev)
+gs = torch.empty((n + 511) // 512, dtype=torch.float64, device=dev)
+out["spmv_full_fused_sumsq_ms"] = timed(lambda: dm.spmv_into(x, y, alpha, 0.0, "tiled",
+                                                              group_sumsq=gs))
+out["partials_from_groups_ms"] = timed(lambda: partials_from_groups(gs, n, 1 << 16))
 out["sumsq_chunks_ms"] = timed(lambda: chunk_partials(y, 1 << 16))
 p = chunk_partials(y, 1 << 16)
 out["fold_ordered_ms"] = timed(lambda: fold_ordered(p))
