@@ -122,6 +122,27 @@ def resolve_variant(variant):
         "or a ParallelRowBlock")
 
 
+# rows the tiled layout may leave to its warp-per-row pass before the
+# selection falls back (rows with more than 15 entries inside one column
+# tile: dense rows in a narrow band)
+TILED_MAX_LEFT_OUT = 0.01
+
+
+def _tiled_layout_fits(dm):
+    """The selection picked TILED from the gather scatter; build its layout
+    (needed anyway) and keep it only if nearly every row is in it."""
+    ok = getattr(dm, "_tiled_fits", None)
+    if ok is None:
+        dm.plan_for("tiled")
+        info = dm.tiles_info()
+        ok = info["n_ovf"] <= TILED_MAX_LEFT_OUT * max(1, dm.row_end - dm.row_start)
+        if not ok:
+            dm._tiled = None  # release the layout
+            dm._invalidate_launches()
+        dm._tiled_fits = ok
+    return ok
+
+
 def kernel_for(dm, kname, order):
     """Concrete kernel name for a resolved (name, order) on this matrix."""
     if kname == "exact":
@@ -130,6 +151,8 @@ def kernel_for(dm, kname, order):
         if dm.stats is None:
             return "staged"
         kname = _CODE_NAME[_native.lib().dacsr_select_variant(dm.stats, order)]
+        if kname == "tiled" and dm.plan is not None and not _tiled_layout_fits(dm):
+            kname = "sliced_pipe"
     if kname in ("wstream", "tiled") + _SLICED and order in (_native.ORDER_MACC3,
                                                              _native.ORDER_STRIP4):
         kname = "rowblock"  # warp streams / slices / tiles specialise the naive order

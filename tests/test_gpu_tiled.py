@@ -218,3 +218,25 @@ def test_fused_group_sumsq(cuda):
     assert not dm.fused_sumsq_ok("sliced_pipe")
     with pytest.raises(DeviceError):
         dm.spmv_into(x, y3, alpha, 0.0, "sliced_pipe", 0, group_sumsq=gs2)
+
+
+def test_selection_falls_back_when_rows_do_not_fit_the_tiles(cuda):
+    """Dense rows in a narrow random band: the gathers are scattered (the
+    statistic says TILED) but most rows hold more than 15 entries inside one
+    column tile and would be left to the warp-per-row pass — the default
+    selection builds the layout, sees that, and runs SLICED_PIPE instead."""
+    from paper_2307_06305_b200.spmv import kernel_for
+    n = 1 << 15
+    arr = banded_arrays(n, 1000, 40.0, 64, 8, cuda, kinds=("da",))
+    dm = DeviceMatrix("da", n, n, arr["rowptr"], arr["offsets"], arr["values"])
+    assert dm.stats.scatter > 0.5
+    assert kernel_for(dm, "exact", 0) == "sliced_pipe" and dm._tiled is None
+    x = normal_vector(n, 4, cuda)
+    y = dg.spmv(dm, x)
+    ref = oracle.spmv("da", arr["rowptr"].cpu().numpy(), arr["offsets"].cpu().numpy(),
+                      arr["values"].cpu().numpy(), x.cpu().numpy())
+    assert np.array_equal(bits(y.cpu().numpy()), bits(ref))
+    # the explicit variant still runs the tiled kernel (left-out rows and all)
+    y2 = dg.spmv(dm, x, variant="tiled")
+    assert dm.tiles_info()["n_ovf"] > n // 2
+    assert np.array_equal(bits(y2.cpu().numpy()), bits(ref))
