@@ -369,7 +369,15 @@ def bench_main(args, rank, world, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    # a failed or hung collective aborts the communicator and raises in
+    # every rank (instead of blocking the stream for ever); the watchdog's
+    # limit is generous against the matrix build and tight against a hang
+    import datetime
+    import os
+    os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+    dist.init_process_group(
+        "nccl", device_id=dev,
+        timeout=datetime.timedelta(seconds=int(os.environ.get("DACSR_NCCL_TIMEOUT_S", "600"))))
     n, b, lam, kmax, seed = BANDED_CONFIGS["c5"]
     chunk = 1 << 16
     iters = 50
@@ -442,8 +450,10 @@ def bench_main(args, rank, world, local):
                                    "clip(Poisson(8),1,32), DA-CSR i16 f64",
                        "nnz": nnz, "bytes_per_spmv": traffic, "iters_per_step": iters,
                        "parallelism": f"row blocks x{world}, +-{b}-row halo (NCCL send/recv "
-                                      "overlapped with the interior rows), norm: one "
-                                      "all_gather of 2^16-row chunk partials",
+                                      "overlapped with the interior rows), norm: sums of "
+                                      "y^2 by 512-row groups out of the SpMV epilogue"
+                                      + ("" if op.fused else " (not fused here)") +
+                                      ", one all_gather of 2^16-row chunk partials",
                        "kernel": op.kernels[0], "build_s": round(build_s, 1),
                        "final_norm": norms[-1],
                        "iterate_sha256": digest,
