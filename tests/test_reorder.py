@@ -76,3 +76,25 @@ def test_adjacency_and_errors():
         dg.permute_symmetric(a, dg.Permutation.identity(3))
     with pytest.raises(ValueError):
         dg.Permutation(np.array([0, 0]), np.array([0, 1]))
+
+
+def test_da_input_is_reordered_by_its_absolute_pattern():
+    """The reference's reorder functions read ``a.colids`` as columns
+    (reorder.py:78-79, 213-214), which for a DacsrMatrix are offsets: there,
+    DA-CSR input is silently treated as a different matrix.  Here the DA
+    offsets are turned back into absolute columns first (a deliberate
+    difference): RCM of a DA-CSR matrix is the RCM of the
+    matrix it stores, and permuting it equals converting the permuted CSR."""
+    from paper_2307_06305_b200.workloads import laplacian_2d
+    rng = np.random.default_rng(5)
+    a = laplacian_2d(12)
+    shuffle = dg.Permutation.from_new_to_old(rng.permutation(a.nrows))
+    b = dg.permute_symmetric(a, shuffle)          # a wide-band CSR matrix
+    d = dg.to_dacsr(b, 16)
+    p_csr, p_da = dg.rcm(b), dg.rcm(d)
+    assert np.array_equal(p_csr.perm, p_da.perm)
+    adj_c, adj_d = dg.symmetrized_adjacency(b), dg.symmetrized_adjacency(d)
+    assert np.array_equal(adj_c.indptr, adj_d.indptr) and np.array_equal(adj_c.indices, adj_d.indices)
+    out = dg.permute_symmetric(d, p_da)
+    assert isinstance(out, dg.DacsrMatrix) and out.iindex_width == 16
+    assert dg.to_csr(out, 32) == dg.permute_symmetric(b, p_csr)
