@@ -374,8 +374,12 @@ int dacsr_spmv_host_streamed(const dacsr_matrix_t* a, const dacsr_plan_t* plans,
 int dacsr_scale(void* y, int32_t values_dtype, int64_t n, double beta, void* stream);
 
 /* Deterministic sum of squares: partial[c] = sum over rows [c*chunk,
- * (c+1)*chunk) ∩ [0, n) of y^2 (fixed tree per chunk, independent of how
- * rows are spread over ranks when rank boundaries are chunk-aligned). */
+ * (c+1)*chunk) ∩ [0, n) of y^2 in a fixed tree, independent of how rows are
+ * spread over ranks when rank boundaries are chunk-aligned.  The tree: the
+ * chunk is cut into groups of 512 values from its start; in a group lane l
+ * (0..31) folds y[32j + l]^2 for j = 0..15 in order, a 5-step xor butterfly
+ * (offsets 16, 8, 4, 2, 1) over the lanes gives the group's sum, and the
+ * groups' sums are folded left to right. */
 int dacsr_sumsq_chunks(const void* y, int32_t values_dtype, int64_t n, int64_t chunk,
                        double* partial, void* stream);
 /* out[0] = sum of partial[0..m) in index order (one thread, exact order). */

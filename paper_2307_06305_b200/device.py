@@ -599,6 +599,9 @@ class DeviceMatrix:
         else:
             sp = stream.cuda_stream
         if group_sumsq is not None:
+            if not isinstance(alpha, torch.Tensor):
+                raise TypeError("group_sumsq needs alpha as a one-element float64 CUDA tensor "
+                                "(dacsr_spmv_dev_alpha_sumsq reads it on the device)")
             status = self._spmv_dev_alpha_sumsq_fn(desc, plan_ref, code, order_code,
                                                    x.data_ptr() if x is not None else None,
                                                    x_offset, y.data_ptr(), alpha.data_ptr(), beta,
