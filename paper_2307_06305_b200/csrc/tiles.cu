@@ -107,6 +107,44 @@ __device__ __forceinline__ uint64_t balance_lanes(const int (&c)[kRowsPerLane], 
     tot += __shfl_sync(0xffffffffu, c[j], lane ^ bm);
     mw |= static_cast<uint64_t>(bm) << (4 * j);
   }
+  // refinement: each row slot's mask chosen again against all the others
+  // (same key; a tie keeps the current mask).  Three sweeps take the lane
+  // utilisation of a C3 tile from 0.88 to 0.90, of a C5 tile from 0.83 to
+  // 0.86 (simulated on Poisson counts; every step saved is a step of the
+  // whole warp).
+#ifndef DACSR_TILES_SWEEPS
+#define DACSR_TILES_SWEEPS 3
+#endif
+#pragma unroll 1
+  for (int sweep = 0; sweep < DACSR_TILES_SWEEPS; ++sweep) {
+    bool changed = false;
+#pragma unroll
+    for (int j = 0; j < kRowsPerLane; ++j) {
+      if (!__any_sync(0xffffffffu, c[j] != 0)) continue;
+      const int cur = static_cast<int>((mw >> (4 * j)) & 15u);
+      const int base = tot - __shfl_sync(0xffffffffu, c[j], lane ^ cur);
+      unsigned long long best = ~0ull;
+      int bm = cur;
+#pragma unroll 1
+      for (int k = 0; k < 16; ++k) {
+        const int m = k == 0 ? cur : (k <= cur ? k - 1 : k);  // the current mask first
+        const int t2 = base + __shfl_sync(0xffffffffu, c[j], lane ^ m);
+        const unsigned mx = __reduce_max_sync(0xffffffffu, static_cast<unsigned>((t2 + G - 1) / G));
+        const unsigned sq = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(t2 * t2));
+        const unsigned long long key = (static_cast<unsigned long long>(mx) << 32) | sq;
+        if (key < best) {
+          best = key;
+          bm = m;
+        }
+      }
+      if (bm != cur) {
+        changed = true;
+        mw = (mw & ~(15ull << (4 * j))) | (static_cast<uint64_t>(bm) << (4 * j));
+      }
+      tot = base + __shfl_sync(0xffffffffu, c[j], lane ^ bm);
+    }
+    if (!changed) break;
+  }
   total = tot;
   return mw;
 }
