@@ -423,7 +423,9 @@ int dacsr_csr_to_da(const dacsr_matrix_t* a, void* offsets, int32_t offsets_dtyp
                     void* stream);
 
 /* ---- seeded C3/C5 generator (oracle: oracle/gen_oracle.c) ----------------- */
-/* counts[r - r0] = entries of row r (diagonal included). */
+/* counts[r - r0] = entries of row r (diagonal included).  1 <= kmax <= 64
+ * and kmax - 1 <= 2b (a row draws up to kmax - 1 distinct non-zero offsets
+ * from [-b, b]); DACSR_ERR_ARG otherwise. */
 int dacsr_gen_banded_counts(int64_t n, int64_t b, int32_t kmax, uint64_t seed,
                             const double* cdf_dev, int64_t r0, int64_t r1, int32_t* counts,
                             void* stream);

@@ -249,6 +249,8 @@ def gen_value(b, seed, r, off, table):
 
 
 def gen_counts(n, b, kmax, seed, cdf, r0, r1):
+    if kmax - 1 > 2 * b:
+        raise ValueError("kmax - 1 distinct non-zero offsets do not exist in [-b, b]")
     out = np.empty(r1 - r0, np.int32)
     lib().orc_gen_counts(n, b, kmax, seed, _p(cdf), r0, r1, _p(out))
     return out

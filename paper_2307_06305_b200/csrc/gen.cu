@@ -131,7 +131,9 @@ extern "C" {
 
 int dacsr_gen_banded_counts(int64_t n, int64_t b, int32_t kmax, uint64_t seed, const double* cdf,
                             int64_t r0, int64_t r1, int32_t* counts, void* stream) {
-  if (b <= 0 || kmax < 1 || kmax > 64 || !cdf || r0 < 0 || r1 < r0 || r1 > n || (r1 > r0 && !counts))
+  // kmax - 1 distinct non-zero offsets must exist in [-b, b]
+  if (b <= 0 || kmax < 1 || kmax > 64 || kmax - 1 > 2 * b || !cdf || r0 < 0 || r1 < r0 || r1 > n ||
+      (r1 > r0 && !counts))
     return DACSR_ERR_ARG;
   if (r1 == r0) return DACSR_OK;
   counts_kernel<<<grid_rows(r1 - r0), 128, 0, static_cast<cudaStream_t>(stream)>>>(
@@ -143,7 +145,8 @@ int dacsr_gen_banded_fill(int64_t n, int64_t b, int32_t kmax, uint64_t seed, con
                           const double* table, int64_t r0, int64_t r1, const void* rowptr,
                           int32_t rdt, int16_t* offsets, int32_t* colids, void* values,
                           int32_t vdt, void* stream) {
-  if (b <= 0 || kmax < 1 || kmax > 64 || !cdf || !table || r0 < 0 || r1 < r0 || r1 > n || !rowptr ||
+  if (b <= 0 || kmax < 1 || kmax > 64 || kmax - 1 > 2 * b || !cdf || !table || r0 < 0 || r1 < r0 ||
+      r1 > n || !rowptr ||
       !values)
     return DACSR_ERR_ARG;
   if (r1 == r0) return DACSR_OK;

@@ -77,3 +77,26 @@ def test_slices_arg_validation_without_device():
                         1.0, 0.0, 0, 64, None) == 5
     assert L.dacsr_spmv(ctypes.byref(m), ctypes.byref(p), _native.VARIANT_CODES["sliced"], 0, x,
                         0, x, 1.0, 0.0, 0, 64, None) == 5
+
+
+def test_generator_and_fused_norm_arg_validation_without_device():
+    """A row draws up to kmax - 1 distinct non-zero offsets from [-b, b]: the
+    generator refuses kmax - 1 > 2b (it would never finish) before any CUDA
+    call; so do the fused-norm entry points on bad arguments."""
+    L = _native.lib()
+    p = ctypes.c_void_p(8)
+    assert L.dacsr_gen_banded_counts(512, 1, 4, 1, p, 0, 512, p, None) == 1
+    assert L.dacsr_gen_banded_counts(512, 1, 65, 1, p, 0, 512, p, None) == 1
+    assert L.dacsr_gen_banded_fill(512, 1, 4, 1, p, p, 0, 512, p, _native.I32, p, None, p,
+                                   _native.F64, None) == 1
+    # chunk not a multiple of 512 / null pointers
+    assert L.dacsr_sumsq_from_groups(p, 4096, 1000, p, None) == 1
+    assert L.dacsr_sumsq_from_groups(None, 4096, 1024, p, None) == 1
+    assert L.dacsr_sumsq_from_groups(None, 0, 1024, None, None) == 0
+    m = _native.Matrix(_native.KIND_DA, _native.I32, _native.I16, _native.F64, 1024, 1024, 100,
+                       16, 32, 64)
+    # group sums exist on the TILED kernel only; null group buffer
+    assert L.dacsr_spmv_dev_alpha_sumsq(ctypes.byref(m), None, _native.VARIANT_CODES["sliced"], 0,
+                                        p, 0, p, p, 0.0, 0, 1024, p, None) == 3
+    assert L.dacsr_spmv_dev_alpha_sumsq(ctypes.byref(m), None, _native.VARIANT_CODES["tiled"], 0,
+                                        p, 0, p, p, 0.0, 0, 1024, None, None) == 1
