@@ -35,12 +35,15 @@ while time.time() < t_end:
     kmax = min(int(rng.choice([1, 4, 32, 64])), 2 * b + 1)  # kmax - 1 distinct offsets in [-b, b]
     seed = int(rng.integers(1, 1 << 30))
     print("case", n, b, lam, kmax, seed, flush=True)
-    arr = banded_arrays(n, b, lam, kmax, seed, dev, kinds=("da", "csr"))
+    vdt = torch.float32 if rng.random() < 0.35 else torch.float64
+    ndt = np.float32 if vdt == torch.float32 else np.float64
+    bits_t = np.uint32 if vdt == torch.float32 else np.uint64
+    arr = banded_arrays(n, b, lam, kmax, seed, dev, kinds=("da", "csr"), values_dtype=vdt)
     rp = arr["rowptr"].cpu().numpy()
     offs, cols, vals = (arr[k].cpu().numpy() for k in ("offsets", "colids", "values"))
     pad = int(rng.choice([0, 5, 64]))
-    x = normal_vector(n, int(rng.integers(1, 1000)), dev)
-    x_ext = torch.zeros(n + 2 * pad, dtype=torch.float64, device=dev)
+    x = normal_vector(n, int(rng.integers(1, 1000)), dev).to(vdt)
+    x_ext = torch.zeros(n + 2 * pad, dtype=vdt, device=dev)
     x_ext[pad:pad + n] = x
     xh = x.cpu().numpy()
     for kind, inner, ih in (("da", "offsets", offs), ("csr", "colids", cols)):
@@ -50,7 +53,7 @@ while time.time() < t_end:
             if rng.random() < 0.3:
                 r0, r1 = 0, n
             alpha, beta = [(1.0, 0.0), (0.7, -0.3), (2.0, 1.0), (-1.5, 0.5)][int(rng.integers(0, 4))]
-            y0 = rng.uniform(-1, 1, n)
+            y0 = rng.uniform(-1, 1, n).astype(ndt)
             want = oracle.spmv_kernel(kind, rp, ih, vals, xh, y0.copy(), alpha, beta,
                                       row_start=r0, row_end=r1)
             for k in KERNELS + ("default",):
@@ -74,17 +77,17 @@ while time.time() < t_end:
                     continue
                 cases += 1
                 torch.cuda.synchronize()
-                if not np.array_equal(y.cpu().numpy().view(np.uint64), want.view(np.uint64)):
+                if not np.array_equal(y.cpu().numpy().view(bits_t), want.view(bits_t)):
                     fails += 1
-                    print("MISMATCH", k, kind, n, b, lam, kmax, seed, r0, r1, alpha, beta, pad,
-                          flush=True)
+                    print("MISMATCH", k, kind, str(vdt), n, b, lam, kmax, seed, r0, r1, alpha, beta,
+                          pad, flush=True)
         # fused group sums on whole-group ranges
         if kind == "da" and n >= 1024:
             dm.build_tiles()
             if dm.fused_sumsq_ok("tiled"):
                 a_dev = torch.tensor([0.9], dtype=torch.float64, device=dev)
                 gs = torch.empty((n + 511) // 512, dtype=torch.float64, device=dev)
-                y = torch.empty(n, dtype=torch.float64, device=dev)
+                y = torch.empty(n, dtype=vdt, device=dev)
                 dm.spmv_into(x, y, a_dev, 0.0, "tiled", 0, group_sumsq=gs)
                 f = partials_from_groups(gs, n, 4096).cpu().numpy()
                 d = chunk_partials(y, 4096).cpu().numpy()
