@@ -155,6 +155,18 @@ def chunk_counts(part, chunk):
     return [-(-(b - a) // chunk) for a, b in part.bounds]
 
 
+def launch_ranges(n_local, b, group=512):
+    """Row ranges of a rank's three SpMV launches, interior first:
+    [(cut0, cut1), (0, cut0), (cut1, n_local)].  The interior rows need no
+    halo (rows >= b and < n_local - b); the cuts sit on ``group``-row
+    boundaries (a few rows that need no halo join the strips) so that every
+    launch covers whole 512-row groups: the TILED epilogue then returns the
+    groups' sums of y^2 (no second pass over y for the norm)."""
+    cut0 = min((b + group - 1) // group * group, n_local)
+    cut1 = max(cut0, (n_local - b) // group * group)
+    return [(cut0, cut1), (0, cut0), (cut1, n_local)]
+
+
 class CudaLocalOp:
     """A rank's rows as DeviceMatrix objects (boundary strips + interior,
     each with its own plan) over one set of arrays."""
@@ -168,13 +180,7 @@ class CudaLocalOp:
         self.plan = plan
         self.chunk = chunk
         self.kind = kind
-        # interior rows need no halo; the cuts sit on 512-row group
-        # boundaries (a few rows that need no halo join the strips) so that
-        # every launch covers whole groups: the TILED epilogue then returns
-        # the groups' sums of y^2 (no second pass over y for the norm)
-        cut0 = min((b + 511) // 512 * 512, n_local)
-        cut1 = max(cut0, (n_local - b) // 512 * 512)
-        self.ranges = [(cut0, cut1), (0, cut0), (cut1, n_local)]  # interior first
+        self.ranges = launch_ranges(n_local, b)
         name, order = resolve_variant(variant)
         self.order = order
         self.mats = []

@@ -129,3 +129,18 @@ def test_gloo_two_ranks_bit_identical_to_one():
     xr, nr = _reference_power_iteration()
     assert np.array_equal(np.array(nr), n1[0])
     assert np.array_equal(xr.view(np.uint64), x1.view(np.uint64))
+
+
+def test_launch_ranges_cover_rows_on_group_boundaries():
+    """A rank's interior / strip launches: disjoint, covering, the interior
+    free of halo rows, every cut a multiple of 512 (fused group sums)."""
+    for n_local in (0, 100, 512, 65536, 1 << 20, (1 << 20) + 65536):
+        for b in (1, 511, 512, 3000, 32767, 1 << 21):
+            (i0, i1), (a0, a1), (c0, c1) = D.launch_ranges(n_local, b)
+            assert a0 == 0 and a1 == i0 and i1 == c0 and c1 == n_local and i0 <= i1
+            assert i0 % 512 == 0 or i0 == n_local
+            assert i1 % 512 == 0 or i1 == i0
+            if i1 > i0:  # interior rows read no halo
+                assert i0 >= b and i1 <= n_local - b
+            # the strips are as thin as the group grid allows
+            assert i0 <= min(n_local, b + 511) and (i1 == i0 or i1 > n_local - b - 512)
