@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--variant", default="naive")
     ap.add_argument("--no-suite", action="store_true", help="skip the other configs' lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--suite", default="c1,c2,c2f32,c2bf16,c4,c5slab")
+    ap.add_argument("--suite", default="c1,c2,c2xl,c2f32,c2bf16,c4,c5slab")
     ap.add_argument("--distributed", action="store_true",
                     help="run the N>1 (C5 power iteration, row blocks + halo) path at one rank")
     ap.add_argument("--workload", default="c3", choices=["c3", "c5"],
@@ -342,7 +342,8 @@ def suite_builders():
     from paper_2307_06305_b200.device import DeviceMatrix
     from paper_2307_06305_b200.gen import banded_arrays, normal_vector
     from paper_2307_06305_b200.workloads import (BANDED_CONFIGS, laplacian_2d, laplacian_3d,
-                                                 skewed_rcm_laplacian, uniform_x)
+                                                 laplacian_3d_box, skewed_rcm_laplacian,
+                                                 uniform_x)
     dev = torch.device("cuda")
 
     def host_pair(csr, x, note):
@@ -357,6 +358,14 @@ def suite_builders():
     def c2():
         csr = laplacian_3d(128)
         return host_pair(csr, uniform_x(csr.ncols, 1), "3D 7-pt 128^3 f64 (188 MB DA)")
+
+    def c2xl():
+        # not a BASELINE config: C2's stencil and int16 offsets on a 1024 x 128 x 128
+        # box, 8 times C2's rows — the stencil class well out of L2 (C2 itself
+        # is a 36 us kernel of 1.5 x the L2 size)
+        csr = laplacian_3d_box((1024, 128, 128))
+        return host_pair(csr, uniform_x(csr.ncols, 1),
+                         "3D 7-pt 1024x128x128 f64 (1.50 GB DA; C2's stencil out of L2, extension)")
 
     def c2f32():
         csr = laplacian_3d(128, np.float32)
@@ -387,7 +396,8 @@ def suite_builders():
                 "csr": DeviceMatrix("csr", rows, n, arr["rowptr"], arr["colids"], arr["values"])}
         return mats, normal_vector(n, 21, dev), "C5 rows [0, 2^25): band b=32767, Poisson(8)"
 
-    return {"c1": c1, "c2": c2, "c2f32": c2f32, "c2bf16": c2bf16, "c4": c4, "c5slab": c5slab}
+    return {"c1": c1, "c2": c2, "c2xl": c2xl, "c2f32": c2f32, "c2bf16": c2bf16, "c4": c4,
+            "c5slab": c5slab}
 
 
 def measure_c5(steps, warmup, local=0):

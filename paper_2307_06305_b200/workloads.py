@@ -72,6 +72,14 @@ def laplacian_3d(nx, dtype=np.float64):
     return _stencil_csr((nx, nx, nx), st, 6.0, -1.0, dtype)
 
 
+def laplacian_3d_box(shape, dtype=np.float64):
+    """7-point Laplacian on a box grid ``shape`` = (nz, ny, nx), slowest axis
+    first: the largest offset is ny*nx, so a long thin box (1024, 128, 128)
+    gives C2's stencil and int16 offsets at 8 times C2's size — out of L2."""
+    st = [(0, -1), (1, -1), (2, -1), (0, 0), (2, 1), (1, 1), (0, 1)]
+    return _stencil_csr(tuple(shape), st, 6.0, -1.0, dtype)
+
+
 def uniform_x(n, seed, low=-1.0, high=1.0):
     """x ~ U[low, high) float64 from ``default_rng(seed)``."""
     return np.random.default_rng(seed).uniform(low, high, n)

@@ -35,8 +35,12 @@ for c in configs:
         mats = {"csr": DeviceMatrix.from_host(a), "da": DeviceMatrix.from_host(dg.to_dacsr(a, 16))}
         x = torch.from_numpy(uniform_x(a.ncols, 1)).to(dev)
     else:
-        dt = {"c2f32": np.float32}.get(c, np.float64)
-        csr = laplacian_2d(1024, dt) if c == "c1" else laplacian_3d(128, dt)
+        dt = {"c2f32": np.float32, "c2xlf32": np.float32}.get(c, np.float64)
+        if c in ("c2xl", "c2xlf32"):  # C2's stencil, int16 offsets, 8x the rows: out of L2
+            from paper_2307_06305_b200.workloads import laplacian_3d_box
+            csr = laplacian_3d_box((1024, 128, 128), dt)
+        else:
+            csr = laplacian_2d(1024, dt) if c == "c1" else laplacian_3d(128, dt)
         mats = {"csr": DeviceMatrix.from_host(csr), "da": DeviceMatrix.from_host(dg.to_dacsr(csr, 16))}
         x = torch.from_numpy(uniform_x(csr.ncols, 1).astype(dt)).to(dev)
         if c == "c2bf16":
