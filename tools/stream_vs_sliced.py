@@ -21,12 +21,16 @@ CASES = [("3d 128x128x128", lambda: laplacian_3d_box((128, 128, 128))),
          ("3d 256x128x128", lambda: laplacian_3d_box((256, 128, 128))),
          ("3d 512x128x128", lambda: laplacian_3d_box((512, 128, 128))),
          ("3d 1024x128x128", lambda: laplacian_3d_box((1024, 128, 128))),
+         ("3d 1024x128x128 f32", lambda: laplacian_3d_box((1024, 128, 128), np.float32)),
          ("2d 2048^2", lambda: laplacian_2d(2048)),
          ("2d 4096^2", lambda: laplacian_2d(4096))]
+only = sys.argv[1] if len(sys.argv) > 1 else ""
 for name, build in CASES:
+    if only not in name:
+        continue
     csr = build()
     mats = {"da": DeviceMatrix.from_host(dg.to_dacsr(csr, 16)), "csr": DeviceMatrix.from_host(csr)}
-    x = torch.from_numpy(uniform_x(csr.ncols, 1)).to(dev)
+    x = torch.from_numpy(uniform_x(csr.ncols, 1).astype(csr.values.dtype)).to(dev)
     for kind, dm in mats.items():
         tr = spmv_traffic(dm.nrows, dm.ncols, dm.nnz, StorageWidths(
             dm.oindex_width // 8, dm.iindex_width // 8, dm.scalar_width // 8)).total_bytes
