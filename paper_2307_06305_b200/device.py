@@ -474,12 +474,26 @@ class DeviceMatrix:
                                         for k, v in tried.items()}
         if self._sliced is not None:
             self.set_sliced_l2_prefetch(flag)
+        flags = {}
         for k in candidates:
             if k in ("wstream", "rowblock", "tiled") + SLICED_KERNELS and self.plan is None:
                 continue
-            times[k] = timed(k)
+            if k in SLICED_KERNELS and tune_layout and self.nnz:
+                # the prefetch flag was chosen on the probe kernel; the other
+                # sliced kernel may want the opposite (SLICED has no offset
+                # pipeline and leans on the prefetch), so each is timed both ways
+                both = {}
+                for on in (flag, not flag):
+                    self.set_sliced_l2_prefetch(on)
+                    both[on] = timed(k)
+                flags[k] = min(both, key=both.get)
+                times[k] = both[flags[k]]
+            else:
+                times[k] = timed(k)
         best = min(times, key=times.get)
         self.tuned_kernel = best
+        if best in flags:
+            self.set_sliced_l2_prefetch(flags[best])
         if best not in SLICED_KERNELS and self._sliced is not None:
             self._sliced = None  # the sliced copy of the entries was only built to be timed
         if best != "tiled" and self._tiled is not None:

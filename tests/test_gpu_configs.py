@@ -124,16 +124,16 @@ def test_c4_rcm_and_skew(cuda):
         assert np.array_equal(y.view(np.uint64), ref.view(np.uint64)), variant
 
 
-def test_selection_streams_large_regular_operators(cuda):
+def test_selection_for_large_regular_operators(cuda):
     """4M rows and more of regular rows without scatter (a stencil well out
-    of L2): the default is WSTREAM (TMA-staged warp streams); C2's size
-    stays on SLICED_PIPE.  Both give the oracle's bits."""
+    of L2): the default is SLICED (the sliced layout at 4 CTAs per SM); C2's
+    size stays on SLICED_PIPE.  Both give the oracle's bits."""
     from paper_2307_06305_b200.device import DeviceMatrix
     from paper_2307_06305_b200.spmv import kernel_for
     from paper_2307_06305_b200.workloads import laplacian_3d, laplacian_3d_box, uniform_x
     big = dg.to_dacsr(laplacian_3d_box((256, 128, 128)), 16)
     dm = DeviceMatrix.from_host(big, cuda)
-    assert dm.stats.rows == 1 << 22 and kernel_for(dm, "exact", 0) == "wstream"
+    assert dm.stats.rows == 1 << 22 and kernel_for(dm, "exact", 0) == "sliced"
     x = torch.from_numpy(uniform_x(big.ncols, 3)).to(cuda)
     y = dg.spmv(dm, x)
     ref = oracle.spmv("da", big.rowptr, big.colids, big.values, x.cpu().numpy())

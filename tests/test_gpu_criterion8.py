@@ -65,7 +65,7 @@ def pair(config, device):
     "c2",
     # C2's stencil on a 1024 x 128 x 128 box (1.5 GB, int16 offsets): the
     # stencil class far out of L2, as the reference's criterion asks —
-    # measured DA/CSR 1.09-1.10 cold, 1.15 in back-to-back SpMVs
+    # measured DA/CSR 1.10-1.12 cold, 1.08 in back-to-back SpMVs
     "c2xl",
     # SLICED_PIPE on C4 (5-entry rows, 22 warps/SM) is latency-bound: the
     # best DA/CSR ratio measured 0.996 .. 1.063 cold across runs
