@@ -945,13 +945,29 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
     q.n = w.l > sl.max_len ? -1 : w.l;  // 256 (none) or a medium / long row
     return q;
   };
-  // lane 0: the slice's two arrays into L2 (bulk prefetch)
+  // the slice's two arrays into L2 (bulk prefetch).  The whole warp issues
+  // it with operands the compiler knows warp-uniform (REDUX of values every
+  // lane holds alike): one UBLKPF each.  Issued by lane 0 alone the two
+  // instructions cost a ~20-instruction leader-election loop each — a tenth
+  // of a 7-entry slice's instructions.
+#ifndef DACSR_SLICED_UNIFORM_PF
+#define DACSR_SLICED_UNIFORM_PF 1
+#endif
   auto stage = [&](const Meta& q) {
-    if (lane != 0 || q.width <= 0) return;
-    if (DACSR_SLICED_PREFETCH && !(flags & DACSR_PLAN_NO_L2_PREFETCH)) {
-      prefetch_l2_bulk(sl.v + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(VT)));
-      prefetch_l2_bulk(sl.ci + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(CI)) & ~15u);
+    if (!(DACSR_SLICED_PREFETCH && !(flags & DACSR_PLAN_NO_L2_PREFETCH))) return;
+    if (DACSR_SLICED_UNIFORM_PF) {
+      const int width = static_cast<int>(__reduce_max_sync(0xffffffffu, q.width));
+      if (width <= 0) return;
+      const uint32_t plo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(q.p0));
+      const uint32_t phi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(q.p0 >> 32));
+      const int64_t p0 = static_cast<int64_t>((static_cast<uint64_t>(phi) << 32) | plo);
+      prefetch_l2_bulk(sl.v + p0, static_cast<uint32_t>(32 * width * sizeof(VT)));
+      prefetch_l2_bulk(sl.ci + p0, static_cast<uint32_t>(32 * width * sizeof(CI)) & ~15u);
+      return;
     }
+    if (lane != 0 || q.width <= 0) return;
+    prefetch_l2_bulk(sl.v + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(VT)));
+    prefetch_l2_bulk(sl.ci + q.p0, static_cast<uint32_t>(32 * q.width * sizeof(CI)) & ~15u);
   };
   if constexpr (PIPE) {
     // offsets one slice ahead: the first batch's offsets of the next slice
