@@ -74,8 +74,6 @@ int32_t dacsr_tiles_max_cols(int32_t values_dtype) {
 
 // Selection by row statistics (measured per config):
 //  * scattered gathers (random wide bands, C3/C5): TILED, x staged in smem;
-//  * regular rows, 2^22 rows and more (large stencils): SLICED (the sliced
-//    layout at 4 CTAs per SM);
 //  * everything else with enough rows (stencils, RCM orders, skew: C1, C2,
 //    C4): SLICED_PIPE on the sliced layout (medium / long rows handled
 //    inside the launch);
@@ -90,14 +88,6 @@ int32_t dacsr_select_variant(const dacsr_stats_t* st, int32_t order) {
   if (order == DACSR_ORDER_MACC3 || order == DACSR_ORDER_STRIP4) return DACSR_VARIANT_ROWBLOCK;
   if (st->rows < 4096) return DACSR_VARIANT_SCALAR;
   if (st->scatter > 0.5 && st->mean_len >= 2.0) return DACSR_VARIANT_TILED;
-  // large regular operators (stencils well out of L2; 4M rows and up):
-  // SLICED — the sliced layout without the offset pipeline, 64 registers,
-  // 4 CTAs per SM: with this much to stream the extra resident warps hide
-  // more latency than the pipeline saves (7-10 % faster than SLICED_PIPE
-  // warm and cold, equal to or faster than the TMA-staged WSTREAM;
-  // tools/stream_vs_sliced.py).  Skewed rows (C4) keep the pipeline.
-  if (st->rows >= (int64_t(1) << 22) && st->max_len <= 64 && st->cv_len <= 0.5)
-    return DACSR_VARIANT_SLICED;
   // small regular operators (C1: 5 M entries, L2-resident once warm): the
   // thread-per-row kernel straight from the CSR arrays wins (9.2 against
   // 12.7 us warm, 18.8 against 20.5 cold) and needs no derived layout; from

@@ -124,19 +124,19 @@ def test_c4_rcm_and_skew(cuda):
         assert np.array_equal(y.view(np.uint64), ref.view(np.uint64)), variant
 
 
-def test_selection_for_large_regular_operators(cuda):
-    """4M rows and more of regular rows without scatter (a stencil well out
-    of L2): the default is SLICED (the sliced layout at 4 CTAs per SM); C2's
-    size stays on SLICED_PIPE.  Both give the oracle's bits."""
+def test_large_regular_operator_default_kernel(cuda):
+    """A stencil well out of L2 (4M rows, C2's stencil on a 256 x 128 x 128
+    box): the default stays SLICED_PIPE (with 32-bit slice indices it beats
+    SLICED and WSTREAM at every size measured, tools/stream_vs_sliced.py) and
+    gives the oracle's bits."""
     from paper_2307_06305_b200.device import DeviceMatrix
     from paper_2307_06305_b200.spmv import kernel_for
-    from paper_2307_06305_b200.workloads import laplacian_3d, laplacian_3d_box, uniform_x
+    from paper_2307_06305_b200.workloads import laplacian_3d_box, uniform_x
     big = dg.to_dacsr(laplacian_3d_box((256, 128, 128)), 16)
     dm = DeviceMatrix.from_host(big, cuda)
-    assert dm.stats.rows == 1 << 22 and kernel_for(dm, "exact", 0) == "sliced"
+    assert dm.stats.rows == 1 << 22 and kernel_for(dm, "exact", 0) == "sliced_pipe"
     x = torch.from_numpy(uniform_x(big.ncols, 3)).to(cuda)
-    y = dg.spmv(dm, x)
     ref = oracle.spmv("da", big.rowptr, big.colids, big.values, x.cpu().numpy())
-    assert np.array_equal(y.cpu().numpy().view(np.uint64), ref.view(np.uint64))
-    small = DeviceMatrix.from_host(dg.to_dacsr(laplacian_3d(128), 16), cuda)
-    assert kernel_for(small, "exact", 0) == "sliced_pipe"
+    for variant in ("naive", "sliced", "wstream"):
+        y = dg.spmv(dm, x, variant=variant)
+        assert np.array_equal(y.cpu().numpy().view(np.uint64), ref.view(np.uint64)), variant
