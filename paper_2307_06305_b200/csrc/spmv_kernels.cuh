@@ -1383,7 +1383,7 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       // 63.8 us), on the regular stencils 7-16 % faster
       const bool small = DACSR_SLICED_SMALL && a->nrows < (int64_t(1) << 31) - 64 &&
                          sd->total < (int64_t(1) << 31) - (int64_t(1) << 16) &&
-                         sd->n_medium == 0 && sd->n_long == 0;
+                         (DACSR_SLICED_SMALL > 1 || (sd->n_medium == 0 && sd->n_long == 0));
       const bool pipe = q.variant == DACSR_VARIANT_SLICED_PIPE;
       auto kern = small ? (pipe ? sliced_kernel<KIND, RP, CI, VT, 1, true>
                                 : sliced_kernel<KIND, RP, CI, VT, 0, true>)
