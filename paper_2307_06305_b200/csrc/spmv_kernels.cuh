@@ -377,7 +377,23 @@ __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s
     }
     if (lane == 0) {
       const int n = static_cast<int>(min64(32 * kPer, e - base));
-      for (int k = 0; k < n; ++k) acc.add(scratch[k]);
+      if (s.order == DACSR_ORDER_MACC3 || s.order == DACSR_ORDER_STRIP4) {
+        for (int k = 0; k < n; ++k) acc.add(scratch[k]);
+      } else {
+        // naive order: the bare chain of additions, products read four at a
+        // time (through OrderedAcc::add the fold ran at ~100 cycles per
+        // entry — C4's longest row, 1055 entries, took as long as the rest
+        // of the kernel)
+        double a = acc.a0;
+        int k = 0;
+        for (; k + 4 <= n; k += 4) {
+          const double q0 = scratch[k], q1 = scratch[k + 1], q2 = scratch[k + 2],
+                       q3 = scratch[k + 3];
+          a = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(a, q0), q1), q2), q3);
+        }
+        for (; k < n; ++k) a = __dadd_rn(a, scratch[k]);
+        acc.a0 = a;
+      }
     }
   }
   __syncwarp();
@@ -891,6 +907,20 @@ __device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, co
 #ifndef DACSR_SLICED_SMALL
 #define DACSR_SLICED_SMALL 1
 #endif
+// compiler barrier that names v: code using v stays behind earlier volatile
+// asm and memory operations (no instruction is emitted)
+template <class T>
+__device__ __forceinline__ void pin_after(T& v) {
+  if constexpr (sizeof(T) == 8)
+    asm volatile("" : "+d"(reinterpret_cast<double&>(v))::"memory");
+  else if constexpr (sizeof(T) == 4)
+    asm volatile("" : "+f"(reinterpret_cast<float&>(v))::"memory");
+  else
+    asm volatile("" : "+h"(reinterpret_cast<unsigned short&>(v))::"memory");
+}
+#ifndef DACSR_SLICED_RAW_LATE
+#define DACSR_SLICED_RAW_LATE 1
+#endif
 template <int KIND, class RP, class CI, class VT, int PIPE, bool SMALL>
 __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTune<VT>::minb)
     sliced_kernel(Mat<KIND, RP, CI, VT> m, Scal s, SliceArgs<CI, VT> sl, int64_t rs64, int64_t re64,
@@ -938,9 +968,21 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
     IX p0;
     int width, n;
   };
+  // kLate (8-byte values): the metadata loads are branch-free (the index
+  // clamped, the length load predicated) so that they can sit in the block
+  // of the operator loads, behind the next slice's offset loads; derive()
+  // discards the values of a slice past the end.  4-byte values keep the
+  // branch and the early position (measured: C2-f32 CSR 17.5 against 18.9 us)
+  constexpr bool kLate = DACSR_SLICED_RAW_LATE && PIPE && sizeof(VT) == 8;
   auto load_raw = [&](IX cc) {
     Raw w{0, 0, 256};
-    if (cc < s1) {
+    if constexpr (kLate) {
+      const IX cq = cc < s1 ? cc : s1 - 1;
+      w.a = static_cast<IX>(ldg(sl.ptr + cq));
+      w.b = static_cast<IX>(ldg(sl.ptr + cq + 1));
+      const IX r = row0 + 32 * cc + lane;
+      if (cc < s1 && r >= rs && r < re) w.l = ldg(sl.len + (r - row0));
+    } else if (cc < s1) {
       w.a = static_cast<IX>(ldg(sl.ptr + cc));
       w.b = static_cast<IX>(ldg(sl.ptr + cc + 1));
       const IX r = row0 + 32 * cc + lane;
@@ -948,10 +990,10 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
     }
     return w;
   };
-  auto derive = [&](const Raw& w) {
+  auto derive = [&](const Raw& w, IX cc) {
     Meta q;
     q.p0 = w.a;
-    q.width = static_cast<int>((w.b - w.a) >> 5);
+    q.width = cc < s1 ? static_cast<int>((w.b - w.a) >> 5) : 0;
     q.n = w.l > sl.max_len ? -1 : w.l;  // 256 (none) or a medium / long row
     return q;
   };
@@ -987,8 +1029,8 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
     // are loaded while this slice's gathers and values are in flight, so
     // each slice costs one memory round (gathers + values) instead of two
     // (offsets, then gathers).
-    Meta cur = derive(load_raw(c));
-    Meta nxt = derive(load_raw(c + W));
+    Meta cur = derive(load_raw(c), c);
+    Meta nxt = derive(load_raw(c + W), c + W);
     stage(nxt);
     OT oc[B];
     // f32 values are cheap to hold too: the next slice's first-batch values
@@ -1009,7 +1051,8 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
     load_offsets(cur, oc);
     if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
     for (; c < s1; c += W) {
-      const Raw raw2 = load_raw(c + 2 * W);
+      Raw raw2;
+      if (!kLate) raw2 = load_raw(c + 2 * W);
       const IX r = row0 + 32 * c + lane;
       const VT* xr = KIND == DACSR_KIND_DA ? xb + r : xb;
       asm("" : "+l"(xr));
@@ -1028,6 +1071,16 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
           vv[u] = on ? ldcs(pv + 32 * u) : VT(0);
       }
       load_offsets(nxt, oc);
+      if (kLate) {
+        // the metadata loads share a scoreboard with the offset loads (ptxas
+        // has six): issued ahead of the gathers, the first gather address
+        // waited for them — a memory latency per slice.  Behind the offset
+        // loads they are covered by the wait for the values.
+        asm volatile("" ::: "memory");
+        raw2 = load_raw(c + 2 * W);
+#pragma unroll
+        for (int u = 0; u < B; ++u) pin_after(xv[u]);  // the sums stay behind these loads
+      }
       double acc = 0.0;
 #pragma unroll
       for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, product(vv[u], xv[u]));
@@ -1038,15 +1091,15 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
                                    [&](int j) { return ldcs(pv + 32 * j); }, B, acc);
       }
       if (cur.n >= 0) epilogue(m.y, r, acc, s.a(), s.beta);
-      const Meta nxt2 = derive(raw2);
+      const Meta nxt2 = derive(raw2, c + 2 * W);
       stage(nxt2);
       cur = nxt;
       nxt = nxt2;
     }
     return;
   }
-  Meta cur = derive(load_raw(c));
-  Meta nxt = derive(load_raw(c + W));
+  Meta cur = derive(load_raw(c), c);
+  Meta nxt = derive(load_raw(c + W), c + W);
   stage(nxt);
   if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
   for (; c < s1; c += W) {
@@ -1070,7 +1123,7 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
                                  [&](int j) { return ldg(pi + 32 * j); },
                                  [&](int j) { return ldg(pv + 32 * j); });
     if (cur.n >= 0) epilogue(m.y, r, acc, s.a(), s.beta);
-    const Meta nxt2 = derive(raw2);
+    const Meta nxt2 = derive(raw2, c + 2 * W);
     stage(nxt2);
     cur = nxt;
     nxt = nxt2;
@@ -1377,13 +1430,11 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
                            sd->n_medium, sd->m_nslices, sd->m_total, sd->long_rows, sd->n_long};
       constexpr int warps = 8, threads = 32 * warps;
       const size_t smem = sd->n_long > 0 ? static_cast<size_t>(warps) * 128 * 8 : 0;
-      // 32-bit slice / row / position indices when they fit — for layouts
-      // without medium or long rows: on C4 (skewed rows) the 32-bit
-      // SLICED_PIPE measured 9 % slower than the 64-bit one (69.4 against
-      // 63.8 us), on the regular stencils 7-16 % faster
+      // 32-bit slice / row / position indices when they fit: 7-16 % faster
+      // on the regular stencils, 3 % on C4 (measured 9 % slower there while
+      // C4's longest row still set the kernel's time)
       const bool small = DACSR_SLICED_SMALL && a->nrows < (int64_t(1) << 31) - 64 &&
-                         sd->total < (int64_t(1) << 31) - (int64_t(1) << 16) &&
-                         (DACSR_SLICED_SMALL > 1 || (sd->n_medium == 0 && sd->n_long == 0));
+                         sd->total < (int64_t(1) << 31) - (int64_t(1) << 16);
       const bool pipe = q.variant == DACSR_VARIANT_SLICED_PIPE;
       auto kern = small ? (pipe ? sliced_kernel<KIND, RP, CI, VT, 1, true>
                                 : sliced_kernel<KIND, RP, CI, VT, 0, true>)
@@ -1395,9 +1446,16 @@ int launch(const dacsr_matrix_t* a, const Req& q) {
       const int64_t slots = static_cast<int64_t>(sms) * per_sm;
       const int64_t nsl = ((q.re - sd->row_start + 31) >> 5) - ((q.rs - sd->row_start) >> 5) +
                           sd->m_nslices;
-      // long rows: one warp each, at most 1/8 of the resident CTAs
+      // long rows: DACSR_SLICED_LONG_PER_WARP rows per warp of the side
+      // CTAs, at most 1/8 of the resident CTAs (a side CTA's slot idles once
+      // its rows are done: one row per warp left 34 of C4's 444 slots idle
+      // for most of the kernel)
+#ifndef DACSR_SLICED_LONG_PER_WARP
+#define DACSR_SLICED_LONG_PER_WARP 4
+#endif
+      constexpr int64_t kLongPerCta = static_cast<int64_t>(warps) * DACSR_SLICED_LONG_PER_WARP;
       const int side = sd->n_long > 0
-                           ? static_cast<int>(std::min<int64_t>((sd->n_long + warps - 1) / warps,
+                           ? static_cast<int>(std::min<int64_t>((sd->n_long + kLongPerCta - 1) / kLongPerCta,
                                                                 std::max<int64_t>(1, slots / 8)))
                            : 0;
       const int64_t grid = std::min<int64_t>((nsl + warps - 1) / warps,
