@@ -530,13 +530,30 @@ __global__ void __launch_bounds__(32 * (kTileWarps + 1), 1)
         // two batches in flight: batch i+1's loads are issued before batch i folds
         OW offA[OK * U / 2], offB[OK * U / 2];
         VW valA[VK * U / 2], valB[VK * U / 2];
+        // ptxas puts every operator load of this loop on one scoreboard, and
+        // a scoreboard wait drains all of it: with batch i+1's loads issued
+        // ahead of batch i's first use, that use waited for the loads just
+        // issued (no lead at all; 18 % of the kernel's stall samples sat on
+        // that one instruction).  touch() makes the next batch's load
+        // addresses depend on a word of this batch (or-ed in under a zero
+        // the compiler cannot see), so the wait comes first and covers only
+        // loads issued a whole fold earlier.
+#ifndef DACSR_TILED_TOUCH
+#define DACSR_TILED_TOUCH 1
+#endif
+        const uint32_t zero = static_cast<uint32_t>(ta.T) & 1u;  // T is a multiple of 16
+        auto touch = [&](const OW* off) {
+          if (DACSR_TILED_TOUCH) lp |= static_cast<uint32_t>(off[0]) & zero;
+        };
         int k0 = 0;
         if (kmax > 0) load_batch(0, offA, valA);
         while (k0 < kmax) {
+          touch(offA);
           if (k0 + U < kmax) load_batch((k0 + U) / G, offB, valB);
           fold_batch(k0, offA, valA);
           k0 += U;
           if (k0 >= kmax) break;
+          touch(offB);
           if (k0 + U < kmax) load_batch((k0 + U) / G, offA, valA);
           fold_batch(k0, offB, valB);
           k0 += U;
