@@ -993,7 +993,8 @@ __global__ void __launch_bounds__(256, PIPE ? DACSR_SLICED_PIPE_MINB : SlicedTun
   auto derive = [&](const Raw& w, IX cc) {
     Meta q;
     q.p0 = w.a;
-    q.width = cc < s1 ? static_cast<int>((w.b - w.a) >> 5) : 0;
+    q.width = static_cast<int>((w.b - w.a) >> 5);
+    if constexpr (kLate) q.width = cc < s1 ? q.width : 0;  // clamped loads past the end
     q.n = w.l > sl.max_len ? -1 : w.l;  // 256 (none) or a medium / long row
     return q;
   };
