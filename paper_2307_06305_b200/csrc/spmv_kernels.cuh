@@ -137,7 +137,7 @@ __device__ void long_row(const Mat<KIND, RP, CI, VT>& m, const Scal& s, int64_t 
       const double* buf = scratch + (c & 1) * kLongChunk;
       const int64_t start = c * kLongChunk;
       const int n = static_cast<int>(min64(kLongChunk, len - start));
-      for (int k = 0; k < n; ++k) acc.add(buf[k]);
+      acc.add_many(buf, n);
     }
     __syncthreads();
   }
@@ -377,23 +377,10 @@ __device__ __noinline__ void warp_long_row(const Mat<KIND, RP, CI, VT> m, Scal s
     }
     if (lane == 0) {
       const int n = static_cast<int>(min64(32 * kPer, e - base));
-      if (s.order == DACSR_ORDER_MACC3 || s.order == DACSR_ORDER_STRIP4) {
-        for (int k = 0; k < n; ++k) acc.add(scratch[k]);
-      } else {
-        // naive order: the bare chain of additions, products read four at a
-        // time (through OrderedAcc::add the fold ran at ~100 cycles per
-        // entry — C4's longest row, 1055 entries, took as long as the rest
-        // of the kernel)
-        double a = acc.a0;
-        int k = 0;
-        for (; k + 4 <= n; k += 4) {
-          const double q0 = scratch[k], q1 = scratch[k + 1], q2 = scratch[k + 2],
-                       q3 = scratch[k + 3];
-          a = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(a, q0), q1), q2), q3);
-        }
-        for (; k < n; ++k) a = __dadd_rn(a, scratch[k]);
-        acc.a0 = a;
-      }
+      // (through OrderedAcc::add the fold ran at ~100 cycles per entry:
+      // C4's longest row, 1055 entries, took as long as the rest of the
+      // kernel; add_many folds aligned blocks as bare addition chains)
+      acc.add_many(scratch, n);
     }
   }
   __syncwarp();
