@@ -831,6 +831,40 @@ __device__ __forceinline__ double slice_row_dot(const Mat<KIND, RP, CI, VT>& m, 
   return acc;
 }
 
+// slice_row_dot with the next batch's offsets loaded while this batch's
+// gathers and values are in flight: one memory round per batch instead of
+// two (the medium slices' chains; the main slices of SLICED_PIPE pipeline
+// across slices instead)
+template <int B, class OT, int KIND, class RP, class CI, class VT, class LI, class LV>
+__device__ __forceinline__ double slice_row_dot_pipe(const Mat<KIND, RP, CI, VT>& m, int64_t r,
+                                                     int width, int n, const VT* xr,
+                                                     const LI& li, const LV& lv) {
+  OT o[B];
+#pragma unroll
+  for (int u = 0; u < B; ++u) o[u] = u < n ? static_cast<OT>(li(u)) : OT(0);
+  double acc = 0.0;
+  for (int j = 0; j < width; j += B) {
+    VT vv[B], xv[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const bool on = j + u < n;
+      if (on) m.check(r, 0, static_cast<CI>(o[u]));
+      xv[u] = on ? ldg(elem_addr(xr, o[u])) : VT(0);
+      vv[u] = on ? lv(j + u) : VT(0);
+    }
+    if (j + B < width) {
+#pragma unroll
+      for (int u = 0; u < B; ++u) o[u] = j + B + u < n ? static_cast<OT>(li(j + B + u)) : OT(0);
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, product(vv[u], xv[u]));
+  }
+  return acc;
+}
+
+#ifndef DACSR_SLICED_MEDIUM_PIPE
+#define DACSR_SLICED_MEDIUM_PIPE 1
+#endif
 // Medium slices t = first, first + stride, ... (32 listed rows each; lanes
 // whose row is outside [rs, re) skip), straight from HBM.  Call after
 // griddepcontrol.wait.
@@ -856,9 +890,22 @@ __device__ __forceinline__ void medium_slices(const Mat<KIND, RP, CI, VT>& m, co
     DACSR_CHECK(n <= 0 || p0 + lane + 32 * (n - 1) < sl.m_total);
     const CI* pi = sl.mci + p0 + lane;
     const VT* pv = sl.mv + p0 + lane;
-    const double acc = slice_row_dot<B, OT>(m, r, width, n, xr,
-                                            [&](int j) { return ldcs(pi + 32 * j); },
-                                            [&](int j) { return ldcs(pv + 32 * j); });
+    double acc;
+    if (DACSR_SLICED_MEDIUM_PIPE) {
+      // the slice's two arrays into L2 (its later batches then wait for L2,
+      // not HBM), and one memory round per batch: a medium slice is a chain
+      // of dependent rounds on a warp whose main slices wait behind it
+      if (lane == 0 && width > 0) {
+        prefetch_l2_bulk(sl.mv + p0, static_cast<uint32_t>(32 * width * sizeof(VT)));
+        prefetch_l2_bulk(sl.mci + p0, static_cast<uint32_t>(32 * width * sizeof(CI)) & ~15u);
+      }
+      acc = slice_row_dot_pipe<B, OT>(m, r, width, n, xr,
+                                      [&](int j) { return ldcs(pi + 32 * j); },
+                                      [&](int j) { return ldcs(pv + 32 * j); });
+    } else {
+      acc = slice_row_dot<B, OT>(m, r, width, n, xr, [&](int j) { return ldcs(pi + 32 * j); },
+                                 [&](int j) { return ldcs(pv + 32 * j); });
+    }
     if (n >= 0) epilogue(m.y, r, acc, s.a(), s.beta);
   }
 }
